@@ -1,0 +1,195 @@
+/*
+ * coinfer_b200.h — C ABI of the B200 solver engine for the offloading and
+ * scheduling hot path of arXiv 2206.06304 (IP-SSA, same-sub-task
+ * aggregation, OG optimal grouping, online slot driver).
+ *
+ * The reference is a header-only C++ library (namespace `coinfer`, value
+ * semantics, exceptions).  This ABI is what a foreign caller binds instead:
+ * plain pointers and sizes, structure-of-arrays fp64 inputs, integer status
+ * codes, no exceptions and no C++ or torch types.  The C++ drop-in layer in
+ * include/coinfer/ rebuilds the reference's value types on top of it and
+ * rethrows the reference's exceptions.
+ *
+ * Reference interfaces replaced (all under /root/reference/proj/include/coinfer):
+ *   coinfer_ipssa_batch   <- ip_ssa(const Scenario&, double)           offline_solvers.hpp:219-224
+ *                            detail::try_ip_ssa                          offline_solvers.hpp:192-204
+ *   coinfer_fixed_batch   <- fixed_batch_schedule(const Scenario&, double, size_t)
+ *                                                                       offline_solvers.hpp:208-214
+ *                            detail::try_fixed_batch (+ aggregation)     offline_solvers.hpp:137-188
+ *   coinfer_og_batch      <- og(const Scenario&)                         offline_solvers.hpp:286-388
+ *                            detail::lc_solve (OG fallback)              offline_solvers.hpp:255-276
+ *   coinfer_sweep_batch   <- the CLI's per-instance pair of solves
+ *                            run_offline_solver("IPSSA"/"OG")           tools/coinfer_main.cpp:237-245
+ *   (per-user energies)   <- schedule_metrics(...).per_user_energy      offline_solvers.hpp:627-646
+ *   (contract checks)     <- Scenario::check / DnnProfile::check        core_model.hpp:31-52,80-101
+ *   coinfer_online_run    <- run_episode(OnlineEnv&, TimeWindowPolicy, horizon, seed)
+ *                                                                       online_sim.hpp:131-249,312-371
+ *
+ * Threading: a context owns one CUDA stream and its workspace; calls on one
+ * context must be serialised by the caller (the reference solvers are pure
+ * and reentrant; use one context per host thread).
+ *
+ * Memory: every array in coinfer_users and the output structs is either all
+ * host memory or all device memory of the context's GPU, selected by
+ * coinfer_users.mem.  Host inputs are copied in and outputs copied back
+ * inside the call (synchronously); device arrays are used in place and the
+ * call only enqueues work on the context stream (call coinfer_ctx_synchronize
+ * before reading results).  Profile arrays are always host memory.
+ * Any output pointer may be NULL: that output is then not produced.
+ */
+#ifndef COINFER_B200_H
+#define COINFER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COINFER_ABI_VERSION 1
+
+/* Call-level return codes. */
+#define COINFER_OK 0
+#define COINFER_E_ARG 1         /* null/ill-shaped argument (std::invalid_argument) */
+#define COINFER_E_PROFILE 2     /* DnnProfile::check failed; message in coinfer_last_error */
+#define COINFER_E_CUDA 3        /* CUDA runtime error; message in coinfer_last_error */
+#define COINFER_E_UNSUPPORTED 4 /* shape outside what the kernels were built for */
+
+/* Per-instance status codes (out->status[k]). */
+#define COINFER_ST_OK 0
+#define COINFER_ST_INFEASIBLE 1 /* std::domain_error (see coinfer_status_message) */
+/* std::invalid_argument from Scenario::check, first failing user, first failing test
+   (core_model.hpp:90-99, in that order) */
+#define COINFER_ST_BAD_FREQ 10      /* "scenario: bad frequency range" */
+#define COINFER_ST_NEG_KAPPA 11     /* "scenario: negative kappa" */
+#define COINFER_ST_BAD_RATE 12      /* "scenario: rates must be positive" */
+#define COINFER_ST_NEG_POWER 13     /* "scenario: negative link power" */
+#define COINFER_ST_NEG_ARRIVAL 14   /* "scenario: negative arrival" */
+#define COINFER_ST_EARLY_DEADLINE 15 /* "scenario: deadline before arrival" */
+#define COINFER_ST_SHORT_TABLE 16   /* "scenario: latency table shorter than user count" */
+#define COINFER_ST_ZERO_BOUND 17    /* b == 0: "batch_start_times: b must be >= 1" (invalid_argument) */
+#define COINFER_ST_BOUND_PAST_TABLE 18 /* b > b_max: std::out_of_range "edge_batch_latency: batch size beyond table" */
+
+#define COINFER_MEM_HOST 0
+#define COINFER_MEM_DEVICE 1
+
+/* Largest sub-task count N the kernels are instantiated for. */
+#define COINFER_MAX_SUBTASKS 16
+
+typedef struct coinfer_ctx coinfer_ctx;
+
+/* DnnProfile (core_model.hpp:17-53).  latency is row-major [n][b-1]:
+   latency[(n-1)*b_max + (b-1)] = F_n(b).  Host memory. */
+typedef struct coinfer_profile {
+  int32_t N;
+  int32_t b_max;
+  const double* work;      /* [N]        A_n                 */
+  const double* data_bits; /* [N+1]      B_0..B_N            */
+  const double* latency;   /* [N*b_max]  F_n(b)              */
+} coinfer_profile;
+
+/* A batch of n_inst independent scenarios, each with M users, stored as
+   structure of arrays: field[k*M + m] is user m of instance k (UserSpec,
+   core_model.hpp:56-66, plus Scenario::deadline).  rate_down/power_down are
+   read only by the contract check and may be NULL (treated as valid). */
+typedef struct coinfer_users {
+  int64_t n_inst;
+  int32_t M;
+  int32_t mem; /* COINFER_MEM_HOST or COINFER_MEM_DEVICE, for inputs and outputs */
+  const double* f_min;
+  const double* f_max;
+  const double* kappa;
+  const double* rate_up;
+  const double* power_up;
+  const double* arrival;
+  const double* deadline;
+  const double* rate_down;  /* optional */
+  const double* power_down; /* optional */
+} coinfer_users;
+
+/* SolveResult (offline_solvers.hpp:119-126) in SoA form, plus the per-user
+   energies of schedule_metrics (offline_solvers.hpp:627-646). */
+typedef struct coinfer_ipssa_out {
+  int32_t* status;           /* [n_inst] COINFER_ST_*                                  */
+  int32_t* batch_bound;      /* [n_inst] SolveResult::batch_bound                      */
+  uint8_t* pipeline_feasible;/* [n_inst] SolveResult::pipeline_feasible                */
+  double* energy;            /* [n_inst] SolveResult::energy (total_energy fold)       */
+  uint8_t* split;            /* [n_inst*M] SolveResult::split                          */
+  double* freq;              /* [n_inst*M] Schedule::freq (f_max placeholder, split 0) */
+  double* user_energy;       /* [n_inst*M] ScheduleMetrics::per_user_energy            */
+  int32_t* batch_size;       /* [n_inst*N] SolveResult::batch_size                     */
+} coinfer_ipssa_out;
+
+/* GroupingPlan (offline_solvers.hpp:234-241) in SoA form.  Groups are listed
+   in rising-deadline order g = 0..n_groups-1; group g holds the sorted users
+   order[group_lo[g] .. group_lo[g]+group_size[g]-1].  Per-group arrays have
+   capacity M per instance. */
+typedef struct coinfer_og_out {
+  int32_t* status;          /* [n_inst]                                               */
+  uint8_t* fallback;        /* [n_inst] GroupingPlan::fallback                        */
+  double* energy;           /* [n_inst] GroupingPlan::energy                          */
+  int32_t* n_groups;        /* [n_inst] groups.size()                                 */
+  int32_t* order;           /* [n_inst*M] users sorted by (deadline, id)              */
+  int32_t* group_of_user;   /* [n_inst*M] group index of original user m              */
+  uint8_t* split;           /* [n_inst*M] split of original user m in the plan        */
+  double* freq;             /* [n_inst*M] Schedule::freq of user m                    */
+  double* user_energy;      /* [n_inst*M] per_user_energy of user m                   */
+  int32_t* group_lo;        /* [n_inst*M] first sorted index of group g               */
+  int32_t* group_size;      /* [n_inst*M] member count of group g                     */
+  int32_t* group_b;         /* [n_inst*M] batch bound the group was solved with (0 in fallback) */
+  double* group_deadline;   /* [n_inst*M] GroupingPlan::group_deadline                */
+  double* group_energy;     /* [n_inst*M] GroupingPlan::group_energy                  */
+  int32_t* group_batch_size;/* [n_inst*M*N] realized batch size per sub-task per group */
+} coinfer_og_out;
+
+int coinfer_abi_version(void);
+
+/* Context: one CUDA device, one stream, a workspace.  NULL on failure. */
+coinfer_ctx* coinfer_ctx_create(int device);
+void coinfer_ctx_destroy(coinfer_ctx* ctx);
+/* Use an existing cudaStream_t (passed as void*) instead of the private one;
+   NULL restores the private stream. */
+int coinfer_ctx_set_stream(coinfer_ctx* ctx, void* stream);
+int coinfer_ctx_synchronize(coinfer_ctx* ctx);
+/* Message of the last call-level error on this context ("" if none). */
+const char* coinfer_last_error(const coinfer_ctx* ctx);
+/* The reference's exception message for a per-instance status code and solver
+   ("ipssa", "fixed", "og"). */
+const char* coinfer_status_message(int32_t status, const char* solver);
+/* Number of kernels this context launched so far (for launch accounting). */
+int64_t coinfer_ctx_launch_count(const coinfer_ctx* ctx);
+/* Diagnostic: measured fp64-pipe throughput of the context's GPU in lane
+   operations per second (independent DADD/DMUL/DFMA streams on every SM);
+   the denominator of the engine's roofline (MEASURED_PEAKS.json has none). */
+int coinfer_probe_fp64(coinfer_ctx* ctx, double* lane_ops_per_s);
+
+/* IP-SSA (Alg. 2) for every instance.  deadline[k] is the common batch
+   deadline l of instance k (same memory kind as the users); NULL means the
+   smallest user deadline of the instance, as the CLI does
+   (coinfer_main.cpp:240-243). */
+int coinfer_ipssa_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                        const coinfer_users* users, const double* deadline,
+                        coinfer_ipssa_out* out);
+
+/* Alg. 1 at one assumed batch bound b[k] (fixed_batch_schedule).  deadline
+   may be NULL as above.  status COINFER_ST_INFEASIBLE when some user cannot
+   meet the deadline. */
+int coinfer_fixed_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                        const coinfer_users* users, const double* deadline,
+                        const int32_t* b, coinfer_ipssa_out* out);
+
+/* OG optimal grouping (Alg. 3) for every instance. */
+int coinfer_og_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                     const coinfer_users* users, coinfer_og_out* out);
+
+/* IP-SSA at the smallest deadline AND OG for every instance in one fused
+   pass (the offline Monte Carlo sweep).  Either output may be NULL. */
+int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                        const coinfer_users* users, coinfer_ipssa_out* ipssa,
+                        coinfer_og_out* og);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COINFER_B200_H */

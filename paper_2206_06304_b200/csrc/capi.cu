@@ -1,0 +1,435 @@
+// capi.cu — the extern "C" boundary (include/coinfer_b200.h).
+//
+// No exceptions cross this boundary; errors are return codes plus a
+// per-context message.  There is no CPU solver behind it: every solve runs
+// in the sm_100a kernels, host memory is only staged through.
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/coinfer_b200.h"
+#include "kernels.h"
+
+namespace cfb {
+cudaError_t probe_fp64(cudaStream_t st, double* ops_per_s);
+}
+
+struct coinfer_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // latency table on the device, re-uploaded only when it changes
+  double* d_lat = nullptr;
+  size_t lat_cap = 0;
+  std::vector<double> lat_host;
+  // staging workspace for host-memory calls
+  unsigned char* ws = nullptr;
+  size_t ws_cap = 0;
+};
+
+namespace {
+
+int fail(coinfer_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(coinfer_ctx* ctx, cudaError_t e, const char* what) {
+  return fail(ctx, COINFER_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// DnnProfile::check (core_model.hpp:31-52), same messages.
+int check_profile(coinfer_ctx* ctx, const coinfer_profile* p) {
+  if (!p || !p->work || !p->data_bits || !p->latency)
+    return fail(ctx, COINFER_E_ARG, "profile: null array");
+  if (p->N <= 0) return fail(ctx, COINFER_E_PROFILE, "profile: no sub-tasks");
+  if (p->b_max <= 0) return fail(ctx, COINFER_E_PROFILE, "profile: empty latency row");
+  for (int i = 0; i < p->N; ++i) {
+    if (p->work[i] <= 0.0) return fail(ctx, COINFER_E_PROFILE, "profile: work must be positive");
+    const double* row = p->latency + (size_t)i * p->b_max;
+    if (row[0] <= 0.0) return fail(ctx, COINFER_E_PROFILE, "profile: F_n(1) must be positive");
+    for (int b = 1; b < p->b_max; ++b)
+      if (row[b] < row[b - 1])
+        return fail(ctx, COINFER_E_PROFILE, "profile: F_n(b) must be nondecreasing in b");
+  }
+  for (int n = 0; n <= p->N; ++n)
+    if (p->data_bits[n] < 0.0) return fail(ctx, COINFER_E_PROFILE, "profile: negative data size");
+  if (p->N > COINFER_MAX_SUBTASKS)
+    return fail(ctx, COINFER_E_UNSUPPORTED, "profile: more sub-tasks than COINFER_MAX_SUBTASKS");
+  return COINFER_OK;
+}
+
+cfb::ProfileConst make_const(const coinfer_profile* p) {
+  cfb::ProfileConst P;
+  std::memset(&P, 0, sizeof P);
+  P.N = p->N;
+  P.bmax = p->b_max;
+  double acc = 0.0;
+  P.prefix[0] = 0.0;
+  for (int n = 0; n < p->N; ++n) {
+    P.work[n] = p->work[n];
+    acc += p->work[n];  // left fold, as DnnProfile::total_work / best_partition
+    P.prefix[n + 1] = acc;
+  }
+  for (int n = 0; n <= p->N; ++n) P.bits[n] = p->data_bits[n];
+  return P;
+}
+
+int upload_latency(coinfer_ctx* ctx, const coinfer_profile* p) {
+  const size_t n = (size_t)p->N * p->b_max;
+  if (ctx->lat_host.size() == n && std::memcmp(ctx->lat_host.data(), p->latency, n * 8) == 0)
+    return COINFER_OK;
+  if (n > ctx->lat_cap) {
+    if (ctx->d_lat) cudaFree(ctx->d_lat);
+    ctx->d_lat = nullptr;
+    cudaError_t e = cudaMalloc(&ctx->d_lat, n * 8);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(latency)");
+    ctx->lat_cap = n;
+  }
+  ctx->lat_host.assign(p->latency, p->latency + n);
+  cudaError_t e =
+      cudaMemcpyAsync(ctx->d_lat, ctx->lat_host.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "upload latency");
+  e = cudaStreamSynchronize(ctx->stream);  // lat_host may change on the next call
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "upload latency");
+  return COINFER_OK;
+}
+
+// Host-memory calls: inputs are copied into one device workspace, outputs
+// are produced there and copied back.
+struct Stager {
+  coinfer_ctx* ctx;
+  size_t used = 0;
+  struct Back {
+    void* host;
+    size_t off;
+    size_t bytes;
+  };
+  std::vector<Back> back;
+  struct In {
+    const void* host;
+    size_t off;
+    size_t bytes;
+  };
+  std::vector<In> in;
+  size_t reserve(size_t bytes) {
+    const size_t off = used;
+    used += (bytes + 255) & ~size_t(255);
+    return off;
+  }
+};
+
+template <class T>
+void plan_in(Stager& s, const T*& p, size_t count) {
+  if (!p) return;
+  const size_t off = s.reserve(count * sizeof(T));
+  s.in.push_back({p, off, count * sizeof(T)});
+  p = reinterpret_cast<const T*>(off + 1);  // placeholder, patched after allocation
+}
+
+template <class T>
+void plan_out(Stager& s, T*& p, size_t count) {
+  if (!p) return;
+  const size_t off = s.reserve(count * sizeof(T));
+  s.back.push_back({p, off, count * sizeof(T)});
+  p = reinterpret_cast<T*>(off + 1);
+}
+
+template <class T>
+void patch(unsigned char* base, T*& p) {
+  if (p) p = reinterpret_cast<T*>(base + (reinterpret_cast<uintptr_t>(p) - 1));
+}
+
+int ensure_ws(coinfer_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_cap) return COINFER_OK;
+  if (ctx->ws) cudaFree(ctx->ws);
+  ctx->ws = nullptr;
+  ctx->ws_cap = 0;
+  cudaError_t e = cudaMalloc(&ctx->ws, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
+  ctx->ws_cap = bytes;
+  return COINFER_OK;
+}
+
+void plan_ip_out(Stager& s, coinfer_ipssa_out& o, size_t K, size_t M, size_t N) {
+  plan_out(s, o.status, K);
+  plan_out(s, o.batch_bound, K);
+  plan_out(s, o.pipeline_feasible, K);
+  plan_out(s, o.energy, K);
+  plan_out(s, o.split, K * M);
+  plan_out(s, o.freq, K * M);
+  plan_out(s, o.user_energy, K * M);
+  plan_out(s, o.batch_size, K * N);
+}
+
+void patch_ip_out(unsigned char* b, coinfer_ipssa_out& o) {
+  patch(b, o.status);
+  patch(b, o.batch_bound);
+  patch(b, o.pipeline_feasible);
+  patch(b, o.energy);
+  patch(b, o.split);
+  patch(b, o.freq);
+  patch(b, o.user_energy);
+  patch(b, o.batch_size);
+}
+
+void plan_og_out(Stager& s, coinfer_og_out& o, size_t K, size_t M, size_t N) {
+  plan_out(s, o.status, K);
+  plan_out(s, o.fallback, K);
+  plan_out(s, o.energy, K);
+  plan_out(s, o.n_groups, K);
+  plan_out(s, o.order, K * M);
+  plan_out(s, o.group_of_user, K * M);
+  plan_out(s, o.split, K * M);
+  plan_out(s, o.freq, K * M);
+  plan_out(s, o.user_energy, K * M);
+  plan_out(s, o.group_lo, K * M);
+  plan_out(s, o.group_size, K * M);
+  plan_out(s, o.group_b, K * M);
+  plan_out(s, o.group_deadline, K * M);
+  plan_out(s, o.group_energy, K * M);
+  plan_out(s, o.group_batch_size, K * M * N);
+}
+
+void patch_og_out(unsigned char* b, coinfer_og_out& o) {
+  patch(b, o.status);
+  patch(b, o.fallback);
+  patch(b, o.energy);
+  patch(b, o.n_groups);
+  patch(b, o.order);
+  patch(b, o.group_of_user);
+  patch(b, o.split);
+  patch(b, o.freq);
+  patch(b, o.user_energy);
+  patch(b, o.group_lo);
+  patch(b, o.group_size);
+  patch(b, o.group_b);
+  patch(b, o.group_deadline);
+  patch(b, o.group_energy);
+  patch(b, o.group_batch_size);
+}
+
+constexpr int kSmallMaxM = 255;  // u8 group/bound indices in shared memory
+
+enum class Mode { Solve, Fixed };
+
+int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* users,
+        const double* deadline, const int32_t* bvec, const coinfer_ipssa_out* ip_in,
+        const coinfer_og_out* og_in, Mode mode) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  if (!users) return fail(ctx, COINFER_E_ARG, "users: null");
+  int rc = check_profile(ctx, prof);
+  if (rc != COINFER_OK) return rc;
+  if (users->n_inst < 0 || users->M < 0) return fail(ctx, COINFER_E_ARG, "users: negative size");
+  if (users->mem != COINFER_MEM_HOST && users->mem != COINFER_MEM_DEVICE)
+    return fail(ctx, COINFER_E_ARG, "users: bad mem kind");
+  if (users->M > 0 && users->n_inst > 0 &&
+      (!users->f_min || !users->f_max || !users->kappa || !users->rate_up || !users->power_up ||
+       !users->arrival || !users->deadline))
+    return fail(ctx, COINFER_E_ARG, "users: null input array");
+  if (mode == Mode::Fixed && users->n_inst > 0 && !bvec)
+    return fail(ctx, COINFER_E_ARG, "fixed: null batch-bound array");
+  if (users->n_inst == 0) return COINFER_OK;
+  if (users->M > kSmallMaxM)
+    return fail(ctx, COINFER_E_UNSUPPORTED, "M above the shared-memory solver's limit");
+
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  rc = upload_latency(ctx, prof);
+  if (rc != COINFER_OK) return rc;
+
+  const size_t K = (size_t)users->n_inst, M = (size_t)users->M, N = (size_t)prof->N;
+  cfb::SmallArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.P = make_const(prof);
+  a.lat = ctx->d_lat;
+  a.n_inst = users->n_inst;
+  a.M = users->M;
+  a.fmin = users->f_min;
+  a.fmax = users->f_max;
+  a.kappa = users->kappa;
+  a.ru = users->rate_up;
+  a.pu = users->power_up;
+  a.arr = users->arrival;
+  a.dl = users->deadline;
+  a.rd = users->rate_down;
+  a.pd = users->power_down;
+  a.l_ip = deadline;
+  a.do_ip = ip_in != nullptr;
+  a.do_og = og_in != nullptr;
+  if (ip_in) a.ip = *ip_in;
+  if (og_in) a.og = *og_in;
+  const int32_t* bdev = bvec;
+
+  const bool host = users->mem == COINFER_MEM_HOST;
+  Stager st{ctx};
+  if (host) {
+    plan_in(st, a.fmin, K * M);
+    plan_in(st, a.fmax, K * M);
+    plan_in(st, a.kappa, K * M);
+    plan_in(st, a.ru, K * M);
+    plan_in(st, a.pu, K * M);
+    plan_in(st, a.arr, K * M);
+    plan_in(st, a.dl, K * M);
+    plan_in(st, a.rd, K * M);
+    plan_in(st, a.pd, K * M);
+    plan_in(st, a.l_ip, K);
+    plan_in(st, bdev, K);
+    if (ip_in) plan_ip_out(st, a.ip, K, M, N);
+    if (og_in) plan_og_out(st, a.og, K, M, N);
+    rc = ensure_ws(ctx, st.used);
+    if (rc != COINFER_OK) return rc;
+    unsigned char* b = ctx->ws;
+    patch(b, a.fmin);
+    patch(b, a.fmax);
+    patch(b, a.kappa);
+    patch(b, a.ru);
+    patch(b, a.pu);
+    patch(b, a.arr);
+    patch(b, a.dl);
+    patch(b, a.rd);
+    patch(b, a.pd);
+    patch(b, a.l_ip);
+    patch(b, bdev);
+    if (ip_in) patch_ip_out(b, a.ip);
+    if (og_in) patch_og_out(b, a.og);
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+    }
+  }
+
+  const int grid = (int)(K < (size_t)(1u << 30) ? K : (size_t)(1u << 30));
+  if (mode == Mode::Fixed) {
+    e = cfb::launch_fixed(a, bdev, grid, ctx->stream);
+  } else {
+    // Many instances: 4 warps per CTA and several CTAs per SM.  Few
+    // instances: 8 warps per CTA to spread each instance's chains wider.
+    const int threads = K >= 1024 ? 128 : 256;
+    const int smem = cfb::small_smem_bytes((int)M, (int)N, threads / 32);
+    if (smem > 227 * 1024)
+      return fail(ctx, COINFER_E_UNSUPPORTED, "instance does not fit in shared memory");
+    e = cfb::launch_small(a, threads, grid, ctx->stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+
+  if (host) {
+    for (const auto& x : st.back) {
+      e = cudaMemcpyAsync(x.host, ctx->ws + x.off, x.bytes, cudaMemcpyDeviceToHost, ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+    }
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "solve");
+  }
+  return COINFER_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int coinfer_abi_version(void) { return COINFER_ABI_VERSION; }
+
+coinfer_ctx* coinfer_ctx_create(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  coinfer_ctx* ctx = new coinfer_ctx;
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return nullptr;
+  }
+  ctx->stream = ctx->own;
+  return ctx;
+}
+
+void coinfer_ctx_destroy(coinfer_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_lat) cudaFree(ctx->d_lat);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+int coinfer_ctx_set_stream(coinfer_ctx* ctx, void* stream) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return COINFER_OK;
+}
+
+int coinfer_ctx_synchronize(coinfer_ctx* ctx) {
+  if (!ctx) return COINFER_E_ARG;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "synchronize");
+  return COINFER_OK;
+}
+
+const char* coinfer_last_error(const coinfer_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t coinfer_ctx_launch_count(const coinfer_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int coinfer_probe_fp64(coinfer_ctx* ctx, double* lane_ops_per_s) {
+  if (!ctx || !lane_ops_per_s) return COINFER_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cfb::probe_fp64(ctx->stream, lane_ops_per_s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "probe_fp64");
+  return COINFER_OK;
+}
+
+const char* coinfer_status_message(int32_t status, const char* solver) {
+  const std::string s = solver ? solver : "";
+  switch (status) {
+    case COINFER_ST_OK: return "";
+    case COINFER_ST_INFEASIBLE:
+      if (s == "og") return "baseline: user cannot meet the deadline locally";
+      if (s == "fixed") return "fixed_batch_schedule: user cannot meet the deadline";
+      return "ip_ssa: no batch bound admits every user";
+    case COINFER_ST_BAD_FREQ: return "scenario: bad frequency range";
+    case COINFER_ST_NEG_KAPPA: return "scenario: negative kappa";
+    case COINFER_ST_BAD_RATE: return "scenario: rates must be positive";
+    case COINFER_ST_NEG_POWER: return "scenario: negative link power";
+    case COINFER_ST_NEG_ARRIVAL: return "scenario: negative arrival";
+    case COINFER_ST_EARLY_DEADLINE: return "scenario: deadline before arrival";
+    case COINFER_ST_SHORT_TABLE: return "scenario: latency table shorter than user count";
+    case COINFER_ST_ZERO_BOUND: return "batch_start_times: b must be >= 1";
+    case COINFER_ST_BOUND_PAST_TABLE: return "edge_batch_latency: batch size beyond table";
+  }
+  return "unknown status";
+}
+
+int coinfer_ipssa_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                        const double* deadline, coinfer_ipssa_out* out) {
+  if (!out) return fail(ctx, COINFER_E_ARG, "ipssa: null output");
+  return run(ctx, profile, users, deadline, nullptr, out, nullptr, Mode::Solve);
+}
+
+int coinfer_fixed_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                        const double* deadline, const int32_t* b, coinfer_ipssa_out* out) {
+  if (!out) return fail(ctx, COINFER_E_ARG, "fixed: null output");
+  return run(ctx, profile, users, deadline, b, out, nullptr, Mode::Fixed);
+}
+
+int coinfer_og_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                     coinfer_og_out* out) {
+  if (!out) return fail(ctx, COINFER_E_ARG, "og: null output");
+  return run(ctx, profile, users, nullptr, nullptr, nullptr, out, Mode::Solve);
+}
+
+int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                        coinfer_ipssa_out* ipssa, coinfer_og_out* og) {
+  if (!ipssa && !og) return fail(ctx, COINFER_E_ARG, "sweep: no output requested");
+  return run(ctx, profile, users, nullptr, nullptr, ipssa, og, Mode::Solve);
+}
+
+}  // extern "C"

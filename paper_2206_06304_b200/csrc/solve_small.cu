@@ -1,0 +1,750 @@
+// solve_small.cu — fused IP-SSA + OG solver, one CTA per problem instance,
+// everything resident in shared memory (M up to ~180 users).
+//
+// Reference (all under /root/reference/proj/include/coinfer):
+//   ip_ssa / detail::try_ip_ssa            offline_solvers.hpp:192-224
+//   detail::try_fixed_batch + aggregation  offline_solvers.hpp:137-188
+//   og (sort, G table, DP, backtrack, stitch, lc fallback)
+//                                          offline_solvers.hpp:255-388
+//   total_energy fold                      schedule.hpp:214-231
+//   schedule_metrics per-user energy       offline_solvers.hpp:627-646
+//
+// Algorithm (bit-identical restatement):
+//  * Users are deadline-sorted once; every per-user quantity the reference
+//    recomputes in its inner loops is hoisted into a shared-memory record.
+//  * A "chain" is one (group start i, assumed batch bound b) pair.  For a
+//    fixed chain the per-user split choices do not depend on the group end j
+//    and total_energy is a left fold, so one pass over j = i..M-1 yields the
+//    energies of all groups i..j at that b (the reference re-solves every
+//    (i, j) cell from scratch: O(M^4 N) -> O(M^3 N)).  Bounds b whose
+//    pipeline does not fit dl[i] all give the same all-local plan, so they
+//    collapse into one "all-local" chain keyed with the largest admissible b.
+//    The IP-SSA solve is one more chain set over the users in original order.
+//  * All chains of the instance are laid out flat (IP chains, then row 0,
+//    row 1, ... with b ascending) and cut into warp tasks of 32 lanes, so
+//    lanes stay ~98% busy.  After every step j each row segment of a warp
+//    takes a segmented lexicographic argmin over its lanes (energy asc, b
+//    desc == the reference's descending-b scan with strict '<').  A row that
+//    continues from a task running concurrently writes into a per-warp head
+//    buffer that is merged (in b order) after the round barrier.
+//  * The grouping DP runs in place over the G triangle (S[i][j] replaces
+//    G[i][j]); each stage is a lexicographic (value, prev) min over
+//    (j, prev) pairs split across the CTA.  Backtrack, then every chosen
+//    group is re-derived from its stored b to produce per-user outputs.
+
+#include <climits>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace cfb {
+
+namespace {
+
+__device__ __forceinline__ int tri_idx(int i, int j, int M) {
+  // row-major upper triangle incl. diagonal
+  return i * M - ((i * (i - 1)) >> 1) + (j - i);
+}
+
+struct Layout {
+  // byte offsets
+  int rec, tri, dls, sumlat, headE, fsc;
+  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, misc;
+  int headb, bstar, parent, spsc;
+  int total;
+};
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline Layout make_layout(int M, int N, int W) {
+  Layout L;
+  const int REC = 4 * N + 5;
+  const int T = M * (M + 1) / 2;
+  int o = 0;
+  L.rec = o;     o = align16(o + 8 * M * REC);
+  L.tri = o;     o = align16(o + 8 * T);
+  L.dls = o;     o = align16(o + 8 * M);
+  L.sumlat = o;  o = align16(o + 8 * (M + 1));
+  L.headE = o;   o = align16(o + 8 * W * M);
+  L.fsc = o;     o = align16(o + 8 * M);
+  L.rowoff = o;  o = align16(o + 4 * (M + 2));
+  L.b0 = o;      o = align16(o + 4 * (M + 1));
+  L.order = o;   o = align16(o + 4 * M);
+  L.rank = o;    o = align16(o + 4 * M);
+  L.gid = o;     o = align16(o + 4 * M);
+  L.glo = o;     o = align16(o + 4 * M);
+  L.ghi = o;     o = align16(o + 4 * M);
+  L.headq = o;   o = align16(o + 4 * W);
+  L.headlen = o; o = align16(o + 4 * W);
+  L.misc = o;    o = align16(o + 4 * 16 + 8 * 4);
+  L.headb = o;   o = align16(o + 2 * W * M);
+  L.bstar = o;   o = align16(o + T);
+  L.parent = o;  o = align16(o + T);
+  L.spsc = o;    o = align16(o + M);
+  L.total = o;
+  return L;
+}
+
+// misc slots
+enum { MI_STATUS = 0, MI_IPB = 1, MI_BESTI = 2, MI_NG = 3, MI_OGST = 4, MI_Q = 5 };
+
+}  // namespace
+
+int small_smem_bytes(int M, int N, int W) { return make_layout(M, N, W).total; }
+
+template <int N>
+__global__ void __launch_bounds__(256) solve_small_kernel(SmallArgs a) {
+  using R = Rec<N>;
+  constexpr int REC = R::SIZE;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int M = a.M;
+  const int tid = threadIdx.x, NT = blockDim.x, W = NT >> 5, lane = tid & 31, warp = tid >> 5;
+  const Layout L = make_layout(M, N, W);
+  double* rec = reinterpret_cast<double*>(sm + L.rec);
+  double* tri = reinterpret_cast<double*>(sm + L.tri);
+  double* dls = reinterpret_cast<double*>(sm + L.dls);
+  double* sumlat = reinterpret_cast<double*>(sm + L.sumlat);
+  double* headE = reinterpret_cast<double*>(sm + L.headE);
+  double* fsc = reinterpret_cast<double*>(sm + L.fsc);
+  int* rowoff = reinterpret_cast<int*>(sm + L.rowoff);
+  int* b0s = reinterpret_cast<int*>(sm + L.b0);
+  int* order = reinterpret_cast<int*>(sm + L.order);
+  int* rank = reinterpret_cast<int*>(sm + L.rank);
+  int* gid = reinterpret_cast<int*>(sm + L.gid);
+  int* glo = reinterpret_cast<int*>(sm + L.glo);
+  int* ghi = reinterpret_cast<int*>(sm + L.ghi);
+  int* headq = reinterpret_cast<int*>(sm + L.headq);
+  int* headlen = reinterpret_cast<int*>(sm + L.headlen);
+  int* misc = reinterpret_cast<int*>(sm + L.misc);
+  double* miscd = reinterpret_cast<double*>(sm + L.misc + 64);
+  int16_t* headb = reinterpret_cast<int16_t*>(sm + L.headb);
+  uint8_t* bstar = reinterpret_cast<uint8_t*>(sm + L.bstar);
+  uint8_t* parent = reinterpret_cast<uint8_t*>(sm + L.parent);
+  uint8_t* spsc = reinterpret_cast<uint8_t*>(sm + L.spsc);
+  const ProfileConst& P = a.P;
+  const double INF = dinf();
+
+  for (int64_t k = blockIdx.x; k < a.n_inst; k += gridDim.x) {
+    const size_t base = (size_t)k * M;
+    // ------------------------------------------------------------------ M = 0
+    if (M == 0) {
+      if (tid == 0) {
+        if (a.do_ip) {
+          if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
+          if (a.ip.batch_bound) a.ip.batch_bound[k] = 0;
+          if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = 1;
+          if (a.ip.energy) a.ip.energy[k] = 0.0;
+          if (a.ip.batch_size)
+            for (int n = 0; n < N; ++n) a.ip.batch_size[(size_t)k * N + n] = 0;
+        }
+        if (a.do_og) {
+          if (a.og.status) a.og.status[k] = COINFER_ST_OK;
+          if (a.og.fallback) a.og.fallback[k] = 0;
+          if (a.og.energy) a.og.energy[k] = 0.0;
+          if (a.og.n_groups) a.og.n_groups[k] = 0;
+        }
+      }
+      continue;
+    }
+
+    // ------------------------------------------- phase 0: check, sort, hoist
+    if (tid == 0) misc[MI_STATUS] = INT_MAX;
+    __syncthreads();
+    for (int m = tid; m < M; m += NT) {
+      const size_t x = base + m;
+      const double rd = a.rd ? a.rd[x] : 1.0, pd = a.pd ? a.pd[x] : 0.0;
+      const int code = check_user(a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], rd, a.pu[x], pd,
+                                  a.arr[x], a.dl[x]);
+      if (code != COINFER_ST_OK) atomicMin(&misc[MI_STATUS], m * 32 + code);
+      fsc[m] = a.dl[x];
+    }
+    __syncthreads();
+    int status = misc[MI_STATUS];
+    if (P.bmax < M) status = COINFER_ST_SHORT_TABLE;  // checked before the users
+    else if (status != INT_MAX) status &= 31;
+    else status = COINFER_ST_OK;
+    if (status != COINFER_ST_OK) {
+      if (tid == 0) {
+        if (a.do_ip && a.ip.status) a.ip.status[k] = status;
+        if (a.do_og && a.og.status) a.og.status[k] = status;
+      }
+      __syncthreads();
+      continue;
+    }
+    // stable rank by (deadline, id): std::sort with std::tie (offline_solvers.hpp:292-296)
+    for (int m = tid; m < M; m += NT) {
+      const double d = fsc[m];
+      int r = 0;
+      for (int o = 0; o < M; ++o) {
+        const double e = fsc[o];
+        r += (e < d) || (e == d && o < m);
+      }
+      rank[m] = r;
+      order[r] = m;
+      dls[r] = d;
+      const size_t x = base + m;
+      build_rec<N>(rec + r * REC, P, a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], a.pu[x], a.arr[x], d);
+    }
+    __syncthreads();
+
+    // ---------------------------------------- phase 1: chains per row, init
+    const int nip = a.do_ip ? 1 : 0;
+    const int Q = nip + (a.do_og ? M : 0);
+    // IP-SSA common deadline: caller's, else min_m l_m (coinfer_main.cpp:240-243)
+    const double l_ip = (a.do_ip && a.l_ip) ? a.l_ip[k] : dls[0];
+    for (int q = tid; q < Q; q += NT) {
+      const bool isip = q < nip;
+      const int row = q - nip;
+      const int len = isip ? M : M - row;
+      const double d = isip ? l_ip : dls[row];
+      const int b0 = first_infeasible<N>(a.lat, P.bmax, d, len);
+      b0s[q] = b0;
+      rowoff[q + 1] = b0 < len ? b0 : len;  // cnt, prefix-summed below
+    }
+    for (int sz = tid + 1; sz <= M; sz += NT) {  // sum_latency (offline_solvers.hpp:42-47)
+      double t = 0.0;
+      for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __ldg(a.lat + (size_t)(n - 1) * P.bmax + sz - 1));
+      sumlat[sz] = t;
+    }
+    if (a.do_og)
+      for (int x = tid; x < M * (M + 1) / 2; x += NT) tri[x] = INF;
+    __syncthreads();
+    if (tid == 0) {
+      rowoff[0] = 0;
+      for (int q = 0; q < Q; ++q) rowoff[q + 1] += rowoff[q];
+      miscd[0] = INF;  // IP-SSA best energy
+      misc[MI_IPB] = 0;
+    }
+    __syncthreads();
+
+    // ------------------------------------------------- phase 2: G table rows
+    const int C = rowoff[Q];
+    const int ntask = (C + 31) >> 5;
+    const int rounds = (ntask + W - 1) / W;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int t = rd * W + warp;
+      if (lane == 0) headlen[warp] = 0;
+      if (t < ntask) {
+        const int c = t * 32 + lane;
+        const bool has = c < C;
+        // segment (row) of this lane: largest q with rowoff[q] <= c
+        int lo = 0, hi = Q - 1;
+        const int cc = has ? c : C - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (rowoff[mid] <= cc) lo = mid; else hi = mid - 1;
+        }
+        const int q = lo;
+        const bool isip = q < nip;
+        const int row = q - nip;
+        const int qlo = rowoff[q], qhi = rowoff[q + 1];
+        const int b0q = b0s[q];
+        const int bidx = cc - qlo + 1;
+        const bool allocal = bidx == b0q;
+        const int len = isip ? M : M - row;
+        const double d = isip ? l_ip : dls[row];
+        double s[N];
+        if (!allocal) start_times<N>(a.lat, P.bmax, d, bidx, s);
+        else
+#pragma unroll
+          for (int n = 0; n < N; ++n) s[n] = 0.0;
+        const int seg_start = max(qlo - t * 32, 0);
+        const int seg_end = min(qhi - t * 32, 32);
+        const bool cont = qlo < t * 32;  // only the lane-0 segment can continue
+        const unsigned segmask =
+            (seg_end >= 32 ? kFull : ((1u << seg_end) - 1u)) & ~((1u << seg_start) - 1u);
+        const int steps = __shfl_sync(kFull, len, 0);
+        bool alive = has;
+        double total = 0.0;
+        int offl = 0;
+        for (int kk = 0; kk < steps; ++kk) {
+          if (alive && kk < len) {
+            const int ri = isip ? rank[kk] : row + kk;
+            const double* r = rec + ri * REC;
+            int sp;
+            double f;
+            choose<N>(r, P, s, !allocal, sp, f);
+            if (sp < 0) {
+              alive = false;
+            } else {
+              total = fold<N>(r, sp, f, total);
+              offl += sp < N;
+            }
+          }
+          const int size = kk + 1;
+          const bool cand = alive && kk < len && (!isip || kk == M - 1) &&
+                            (allocal ? (size >= b0q) : (bidx <= size && offl <= bidx));
+          const unsigned bal = __ballot_sync(kFull, cand);
+          double res = INF;
+          int resb = 0;
+          if (bal) {
+            const double e = cand ? total : INF;
+            double mn = e;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const double o = __shfl_down_sync(kFull, mn, off);
+              if (lane + off < seg_end && o < mn) mn = o;
+            }
+            const double mh = __shfl_sync(kFull, mn, seg_start);
+            const unsigned wm = __ballot_sync(kFull, cand && e == mh) & segmask;
+            if (wm) {
+              const int win = 31 - __clz(wm);
+              int wb = t * 32 + win - qlo + 1;
+              if (wb == b0q) wb = size;  // all-local chain: largest admissible b
+              res = mh;
+              resb = wb;
+            }
+          }
+          if (lane == seg_start && kk < len) {
+            if (cont) {
+              headE[warp * M + kk] = res;
+              headb[warp * M + kk] = (int16_t)resb;
+            } else if (res != INF) {
+              if (isip) {
+                miscd[0] = res;
+                misc[MI_IPB] = resb;
+              } else {
+                const int x = tri_idx(row, row + kk, M);
+                tri[x] = res;
+                bstar[x] = (uint8_t)resb;
+              }
+            }
+          }
+        }
+        if (cont && lane == 0) {
+          headq[warp] = q;
+          headlen[warp] = len;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int w = 0; w < W; ++w) {
+          const int hl = headlen[w];
+          if (hl == 0) continue;
+          const int q = headq[w];
+          const bool isip = q < nip;
+          const int row = q - nip;
+          for (int kk = lane; kk < hl; kk += 32) {
+            const double e = headE[w * M + kk];
+            if (e == INF) continue;
+            const int hb = headb[w * M + kk];
+            if (isip) {
+              if (kk == M - 1 && e <= miscd[0]) {
+                miscd[0] = e;
+                misc[MI_IPB] = hb;
+              }
+            } else {
+              const int x = tri_idx(row, row + kk, M);
+              if (e <= tri[x]) {  // later chains carry larger b: they win ties
+                tri[x] = e;
+                bstar[x] = (uint8_t)hb;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    }
+
+    // ------------------------------------------------- phase 3: IP-SSA output
+    if (a.do_ip) {
+      const double ipE = miscd[0];
+      const int ipb = misc[MI_IPB];
+      if (ipE == INF) {
+        if (tid == 0 && a.ip.status) a.ip.status[k] = COINFER_ST_INFEASIBLE;
+      } else {
+        const bool pipe = ipb < b0s[0];
+        double s[N];
+        if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipb, s);
+        else
+#pragma unroll
+          for (int n = 0; n < N; ++n) s[n] = 0.0;
+        for (int m = tid; m < M; m += NT) {
+          const double* r = rec + rank[m] * REC;
+          int sp;
+          double f;
+          choose<N>(r, P, s, pipe, sp, f);
+          const size_t x = base + m;
+          if (a.ip.split) a.ip.split[x] = (uint8_t)sp;
+          if (a.ip.freq) a.ip.freq[x] = f;
+          if (a.ip.user_energy) a.ip.user_energy[x] = fold<N>(r, sp, f, 0.0);
+          spsc[rank[m]] = (uint8_t)sp;
+        }
+        if (tid == 0) {
+          if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
+          if (a.ip.batch_bound) a.ip.batch_bound[k] = ipb;
+          if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = pipe;
+          if (a.ip.energy) a.ip.energy[k] = ipE;
+        }
+        __syncthreads();
+        if (a.ip.batch_size)
+          for (int n = 1 + tid; n <= N; n += NT) {
+            int c = 0;
+            for (int x = 0; x < M; ++x) c += spsc[x] < n;
+            a.ip.batch_size[(size_t)k * N + n - 1] = c;
+          }
+      }
+      __syncthreads();
+    }
+    if (!a.do_og) continue;
+
+    // ---------------------------------------------------- phase 4: OG DP
+    // S[0][j] = G[0][j] already in place.
+    for (int i = 1; i < M; ++i) {
+      const int nj = M - i;
+      int Qp = 1;  // threads per j, power of two <= 32
+      while (Qp < 32 && nj * Qp * 2 <= NT && Qp < i) Qp <<= 1;
+      const int pairs = nj * Qp;
+      const int iters = (pairs + NT - 1) / NT;
+      const double di = dls[i];
+      for (int it = 0; it < iters; ++it) {
+        const int t = it * NT + tid;
+        const bool act = t < pairs;
+        const int j = i + (act ? t / Qp : 0);
+        const int qq = t % Qp;
+        double best = INF;
+        int bp = 255;
+        double g = INF;
+        if (act) {
+          g = tri[tri_idx(i, j, M)];
+          if (g != INF) {
+            const double thr = sumlat[j - i + 1];
+            for (int prev = qq; prev < i; prev += Qp) {
+              // groups_fit (offline_solvers.hpp:229-232); feasible prevs form a prefix
+              if (!(__dadd_rn(dls[prev], thr) <= di)) break;
+              const double sp = tri[tri_idx(prev, i - 1, M)];
+              if (sp == INF) continue;
+              const double cand = __dadd_rn(sp, g);
+              if (cand < best) {
+                best = cand;
+                bp = prev;
+              }
+            }
+          }
+        }
+        // lexicographic (value, prev) min over the Qp threads of this j
+        for (int off = 1; off < Qp; off <<= 1) {
+          const double ob = __shfl_xor_sync(kFull, best, off);
+          const int op = __shfl_xor_sync(kFull, bp, off);
+          if (ob < best || (ob == best && op < bp)) {
+            best = ob;
+            bp = op;
+          }
+        }
+        if (act && qq == 0) {
+          const int x = tri_idx(i, j, M);
+          tri[x] = best;
+          parent[x] = (uint8_t)bp;
+        }
+      }
+      __syncthreads();
+    }
+
+    // best_i: strict '<', smallest i (offline_solvers.hpp:332-334)
+    if (warp == 0) {
+      double bv = INF;
+      int bi = M;
+      for (int i = lane; i < M; i += 32) {
+        const double v = tri[tri_idx(i, M - 1, M)];
+        if (v < bv || (v == bv && i < bi)) {
+          bv = v;
+          bi = i;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, bv, off);
+        const int oi = __shfl_xor_sync(kFull, bi, off);
+        if (ov < bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        misc[MI_BESTI] = (bv == INF) ? -1 : bi;
+        miscd[1] = bv;
+        misc[MI_OGST] = COINFER_ST_OK;
+      }
+    }
+    __syncthreads();
+    const int best_i = misc[MI_BESTI];
+    if (a.og.order)
+      for (int i = tid; i < M; i += NT) a.og.order[base + i] = order[i];
+
+    if (best_i < 0) {
+      // ------------------------------ lc_solve fallback (offline_solvers.hpp:336-348)
+      for (int i = tid; i < M; i += NT) {
+        const double* r = rec + i * REC;
+        if (r[R::FEAS] == 0.0) misc[MI_OGST] = COINFER_ST_INFEASIBLE;
+      }
+      __syncthreads();
+      if (misc[MI_OGST] != COINFER_ST_OK) {
+        if (tid == 0 && a.og.status) a.og.status[k] = COINFER_ST_INFEASIBLE;
+        __syncthreads();
+        continue;
+      }
+      for (int i = tid; i < M; i += NT) {
+        const double* r = rec + i * REC;
+        const double fL = r[R::FL];
+        const double e = fold<N>(r, N, fL, 0.0);
+        const int m = order[i];
+        const size_t g = base + i;
+        if (a.og.group_lo) a.og.group_lo[g] = i;
+        if (a.og.group_size) a.og.group_size[g] = 1;
+        if (a.og.group_b) a.og.group_b[g] = 0;
+        if (a.og.group_deadline) a.og.group_deadline[g] = dls[i];
+        if (a.og.group_energy) a.og.group_energy[g] = e;
+        if (a.og.group_batch_size)
+          for (int n = 0; n < N; ++n) a.og.group_batch_size[g * N + n] = 0;
+        if (a.og.group_of_user) a.og.group_of_user[base + m] = i;
+        if (a.og.split) a.og.split[base + m] = (uint8_t)N;
+        if (a.og.freq) a.og.freq[base + m] = fL;
+        if (a.og.user_energy) a.og.user_energy[base + m] = e;
+      }
+      if (tid == 0) {
+        double total = 0.0;  // lc_solve folds users in original order
+        for (int m = 0; m < M; ++m) {
+          const double* r = rec + rank[m] * REC;
+          total = fold<N>(r, N, r[R::FL], total);
+        }
+        if (a.og.status) a.og.status[k] = COINFER_ST_OK;
+        if (a.og.fallback) a.og.fallback[k] = 1;
+        if (a.og.energy) a.og.energy[k] = total;
+        if (a.og.n_groups) a.og.n_groups[k] = M;
+      }
+      __syncthreads();
+      continue;
+    }
+
+    // ------------------------------- backtrack (offline_solvers.hpp:350-360)
+    if (tid == 0) {
+      int ng = 0, i = best_i, j = M - 1;
+      while (true) {
+        glo[ng] = i;
+        ghi[ng] = j;
+        ++ng;
+        if (i == 0) break;
+        const int prev = parent[tri_idx(i, j, M)];
+        j = i - 1;
+        i = prev;
+      }
+      for (int x = 0, y = ng - 1; x < y; ++x, --y) {
+        int tt = glo[x];
+        glo[x] = glo[y];
+        glo[y] = tt;
+        tt = ghi[x];
+        ghi[x] = ghi[y];
+        ghi[y] = tt;
+      }
+      misc[MI_NG] = ng;
+    }
+    __syncthreads();
+    const int ng = misc[MI_NG];
+    for (int g = tid; g < ng; g += NT)
+      for (int x = glo[g]; x <= ghi[g]; ++x) gid[x] = g;
+    __syncthreads();
+
+    // --------------------------- stitch: re-derive every chosen group's plan
+    for (int j = tid; j < M; j += NT) {
+      const int g = gid[j];
+      const int lo = glo[g], hi = ghi[g];
+      const int bb = bstar[tri_idx(lo, hi, M)];
+      const bool pipe = bb < b0s[nip + lo];
+      double s[N];
+      if (pipe) start_times<N>(a.lat, P.bmax, dls[lo], bb, s);
+      else
+#pragma unroll
+        for (int n = 0; n < N; ++n) s[n] = 0.0;
+      const double* r = rec + j * REC;
+      int sp;
+      double f;
+      choose<N>(r, P, s, pipe, sp, f);
+      spsc[j] = (uint8_t)sp;
+      fsc[j] = f;
+      const int m = order[j];
+      if (a.og.group_of_user) a.og.group_of_user[base + m] = g;
+      if (a.og.split) a.og.split[base + m] = (uint8_t)sp;
+      if (a.og.freq) a.og.freq[base + m] = f;
+      if (a.og.user_energy) a.og.user_energy[base + m] = fold<N>(r, sp, f, 0.0);
+    }
+    __syncthreads();
+    for (int g = tid; g < ng; g += NT) {
+      const int lo = glo[g], hi = ghi[g];
+      double total = 0.0;
+      for (int x = lo; x <= hi; ++x) total = fold<N>(rec + x * REC, spsc[x], fsc[x], total);
+      sumlat[g] = total;  // group energies (sumlat no longer needed)
+      const size_t gi = base + g;
+      if (a.og.group_lo) a.og.group_lo[gi] = lo;
+      if (a.og.group_size) a.og.group_size[gi] = hi - lo + 1;
+      if (a.og.group_b) a.og.group_b[gi] = bstar[tri_idx(lo, hi, M)];
+      if (a.og.group_deadline) a.og.group_deadline[gi] = dls[lo];
+      if (a.og.group_energy) a.og.group_energy[gi] = total;
+      if (a.og.group_batch_size)
+        for (int n = 1; n <= N; ++n) {
+          int c = 0;
+          for (int x = lo; x <= hi; ++x) c += spsc[x] < n;
+          a.og.group_batch_size[gi * N + n - 1] = c;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double e = 0.0;  // plan.energy: left fold of group energies (:385-386)
+      for (int g = 0; g < ng; ++g) e = __dadd_rn(e, sumlat[g]);
+      if (a.og.status) a.og.status[k] = COINFER_ST_OK;
+      if (a.og.fallback) a.og.fallback[k] = 0;
+      if (a.og.energy) a.og.energy[k] = e;
+      if (a.og.n_groups) a.og.n_groups[k] = ng;
+    }
+    __syncthreads();
+  }
+}
+
+// fixed_batch_schedule (offline_solvers.hpp:208-214): one CTA per instance.
+template <int N>
+__global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int32_t* bvec) {
+  using R = Rec<N>;
+  constexpr int REC = R::SIZE;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int M = a.M;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  double* rec = reinterpret_cast<double*>(sm);
+  double* fsc = rec + (size_t)M * REC;
+  int* spsc = reinterpret_cast<int*>(fsc + M);
+  __shared__ int st;
+  __shared__ double lmin;
+  const ProfileConst& P = a.P;
+  for (int64_t k = blockIdx.x; k < a.n_inst; k += gridDim.x) {
+    const size_t base = (size_t)k * M;
+    if (tid == 0) st = INT_MAX;
+    __syncthreads();
+    for (int m = tid; m < M; m += NT) {
+      const size_t x = base + m;
+      const double rd = a.rd ? a.rd[x] : 1.0, pd = a.pd ? a.pd[x] : 0.0;
+      const int code = check_user(a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], rd, a.pu[x], pd,
+                                  a.arr[x], a.dl[x]);
+      if (code != COINFER_ST_OK) atomicMin(&st, m * 32 + code);
+      build_rec<N>(rec + m * REC, P, a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], a.pu[x], a.arr[x],
+                   a.dl[x]);
+    }
+    if (tid == 0) {
+      double l = M ? a.dl[base] : 0.0;
+      for (int m = 0; m < M; ++m) l = smin(l, a.dl[base + m]);
+      lmin = l;
+    }
+    __syncthreads();
+    int status = st;
+    if (P.bmax < M) status = COINFER_ST_SHORT_TABLE;
+    else if (status != INT_MAX) status &= 31;
+    else status = COINFER_ST_OK;
+    const int b = bvec[k];
+    if (status == COINFER_ST_OK && b < 1) status = COINFER_ST_ZERO_BOUND;
+    if (status == COINFER_ST_OK && b > P.bmax) status = COINFER_ST_BOUND_PAST_TABLE;
+    if (status != COINFER_ST_OK) {
+      if (tid == 0 && a.ip.status) a.ip.status[k] = status;
+      __syncthreads();
+      continue;
+    }
+    const double l = a.l_ip ? a.l_ip[k] : lmin;
+    double s[N];
+    const bool pipe = start_times<N>(a.lat, P.bmax, l, b, s);
+    for (int m = tid; m < M; m += NT) {
+      int sp;
+      double f;
+      choose<N>(rec + m * REC, P, s, pipe, sp, f);
+      spsc[m] = sp;
+      fsc[m] = f;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      bool ok = true;
+      for (int m = 0; m < M; ++m) ok = ok && spsc[m] >= 0;
+      st = ok ? COINFER_ST_OK : COINFER_ST_INFEASIBLE;
+    }
+    __syncthreads();
+    if (st != COINFER_ST_OK) {
+      if (tid == 0 && a.ip.status) a.ip.status[k] = st;
+      __syncthreads();
+      continue;
+    }
+    for (int m = tid; m < M; m += NT) {
+      const size_t x = base + m;
+      if (a.ip.split) a.ip.split[x] = (uint8_t)spsc[m];
+      if (a.ip.freq) a.ip.freq[x] = fsc[m];
+      if (a.ip.user_energy) a.ip.user_energy[x] = fold<N>(rec + m * REC, spsc[m], fsc[m], 0.0);
+    }
+    if (a.ip.batch_size)
+      for (int n = 1 + tid; n <= N; n += NT) {
+        int c = 0;
+        for (int m = 0; m < M; ++m) c += spsc[m] < n;
+        a.ip.batch_size[(size_t)k * N + n - 1] = c;
+      }
+    if (tid == 0) {
+      double total = 0.0;
+      for (int m = 0; m < M; ++m) total = fold<N>(rec + m * REC, spsc[m], fsc[m], total);
+      if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
+      if (a.ip.batch_bound) a.ip.batch_bound[k] = b;
+      if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = pipe;
+      if (a.ip.energy) a.ip.energy[k] = total;
+    }
+    __syncthreads();
+  }
+}
+
+int fixed_smem_bytes(int M, int N) { return 8 * M * (4 * N + 5) + 8 * M + 4 * M + 16; }
+
+// ------------------------------------------------------------ host launch
+template <int N>
+static cudaError_t launch_small_n(const SmallArgs& a, int threads, int grid, cudaStream_t st) {
+  const int W = threads / 32;
+  const int smem = small_smem_bytes(a.M, N, W);
+  cudaError_t e = cudaFuncSetAttribute(solve_small_kernel<N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  solve_small_kernel<N><<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st) {
+  const int smem = fixed_smem_bytes(a.M, N);
+  cudaError_t e = cudaFuncSetAttribute(fixed_batch_kernel<N>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  fixed_batch_kernel<N><<<grid, 128, smem, st>>>(a, b);
+  return cudaGetLastError();
+}
+
+#define CFB_DISPATCH_N(NVAL, CALL) \
+  switch (NVAL) {                  \
+    case 1: CALL(1); break;        \
+    case 2: CALL(2); break;        \
+    case 3: CALL(3); break;        \
+    case 4: CALL(4); break;        \
+    case 5: CALL(5); break;        \
+    case 6: CALL(6); break;        \
+    case 7: CALL(7); break;        \
+    case 8: CALL(8); break;        \
+    case 9: CALL(9); break;        \
+    case 10: CALL(10); break;      \
+    case 11: CALL(11); break;      \
+    case 12: CALL(12); break;      \
+    case 13: CALL(13); break;      \
+    case 14: CALL(14); break;      \
+    case 15: CALL(15); break;      \
+    case 16: CALL(16); break;      \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st) {
+#define CFB_CALL(n) return launch_small_n<n>(a, threads, grid, st)
+  CFB_DISPATCH_N(a.P.N, CFB_CALL)
+#undef CFB_CALL
+}
+
+cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st) {
+#define CFB_CALL(n) return launch_fixed_n<n>(a, b, grid, st)
+  CFB_DISPATCH_N(a.P.N, CFB_CALL)
+#undef CFB_CALL
+}
+
+}  // namespace cfb

@@ -1,0 +1,240 @@
+"""Batch solver engine: the Python face of the C ABI (include/coinfer_b200.h).
+
+Inputs are structure-of-arrays batches: every user field is a (n_inst, M)
+float64 array, either numpy (host memory; the call stages it through the
+GPU) or a CUDA torch tensor (device memory; the call enqueues on the
+engine's stream and returns device tensors without synchronising).
+
+All solving happens in the sm_100a kernels of libcoinfer_b200.so; there is
+no CPU code path behind these calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import _abi
+
+try:  # torch is plumbing only (device memory, streams)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+@dataclass
+class ProfileArrays:
+    """DnnProfile in flat form (core_model.hpp:17-53)."""
+    work: np.ndarray        # [N]
+    data_bits: np.ndarray   # [N+1]
+    latency: np.ndarray     # [N, b_max], F_n(b) at [n-1, b-1]
+
+    @property
+    def N(self) -> int:
+        return int(self.work.shape[0])
+
+    @property
+    def b_max(self) -> int:
+        return int(self.latency.shape[1])
+
+
+def as_profile(p) -> ProfileArrays:
+    if isinstance(p, ProfileArrays):
+        return p
+    lat = np.ascontiguousarray(np.asarray(p.latency, dtype=np.float64))
+    if lat.ndim == 1:
+        lat = lat.reshape(len(p.work), -1)
+    return ProfileArrays(np.ascontiguousarray(np.asarray(p.work, dtype=np.float64)),
+                         np.ascontiguousarray(np.asarray(p.data_bits, dtype=np.float64)), lat)
+
+
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _ptr(x, ctype):
+    if x is None:
+        return C.cast(None, C.POINTER(ctype))
+    if _is_torch(x):
+        return C.cast(C.c_void_p(x.data_ptr()), C.POINTER(ctype))
+    return x.ctypes.data_as(C.POINTER(ctype))
+
+
+_CT = {"d": C.c_double, "i": C.c_int32, "u": C.c_uint8}
+_NP = {"d": np.float64, "i": np.int32, "u": np.uint8}
+_TT = {"d": "float64", "i": "int32", "u": "uint8"}
+
+
+def _kind(ctype) -> str:
+    return {C.POINTER(C.c_double): "d", C.POINTER(C.c_int32): "i",
+            C.POINTER(C.c_uint8): "u"}[ctype]
+
+
+class Packed:
+    """ctypes structs for one call plus the arrays they point into."""
+
+    def __init__(self, profile, users: Dict, mem: int, want_ip=True, want_og=False,
+                 device=None, ip_fields=None, og_fields=None, pinned=False):
+        self.pinned = pinned
+        self.p = as_profile(profile)
+        self.keep = [self.p.work, self.p.data_bits, self.p.latency]
+        self.profile = _abi.Profile(self.p.N, self.p.b_max, _ptr(self.p.work, C.c_double),
+                                    _ptr(self.p.data_bits, C.c_double),
+                                    _ptr(self.p.latency, C.c_double))
+        ref = users["deadline"]
+        K, M = int(ref.shape[0]), int(ref.shape[1])
+        self.K, self.M, self.N = K, M, self.p.N
+        ptrs = {}
+        for f in _abi.USER_FIELDS:
+            a = users.get(f)
+            if a is not None:
+                if _is_torch(a):
+                    a = a.contiguous()
+                    assert a.dtype == torch.float64
+                else:
+                    a = np.ascontiguousarray(a, dtype=np.float64)
+                self.keep.append(a)
+            ptrs[f] = _ptr(a, C.c_double)
+        self.users = _abi.Users(K, M, mem, *[ptrs[f] for f in _abi.USER_FIELDS])
+        self.out_ip = self._alloc(_abi.IPSSA_FIELDS, _abi.IpssaOut, ip_fields, mem, device) \
+            if want_ip else None
+        self.out_og = self._alloc(_abi.OG_FIELDS, _abi.OgOut, og_fields, mem, device) \
+            if want_og else None
+
+    def _alloc(self, fields, struct, only, mem, device):
+        dims = {"K": self.K, "KM": self.K * self.M, "KN": self.K * self.N,
+                "KMN": self.K * self.M * self.N}
+        shapes = {"K": (self.K,), "KM": (self.K, self.M), "KN": (self.K, self.N),
+                  "KMN": (self.K, self.M, self.N)}
+        arrays, ptrs = {}, []
+        for name, ctype, dim in fields:
+            k = _kind(ctype)
+            if only is not None and name not in only:
+                ptrs.append(C.cast(None, ctype))
+                continue
+            if mem == _abi.MEM_DEVICE:
+                a = torch.empty(shapes[dim], dtype=getattr(torch, _TT[k]), device=device)
+            elif self.pinned:  # page-locked host outputs: D2H at full PCIe/C2C speed
+                a = torch.empty(shapes[dim], dtype=getattr(torch, _TT[k]), pin_memory=True).numpy()
+            else:
+                a = np.zeros(shapes[dim], dtype=_NP[k])
+            arrays[name] = a
+            ptrs.append(_ptr(a, _CT[k]))
+            assert dims[dim] >= 0
+        s = struct(*ptrs)
+        s._arrays = arrays
+        return s
+
+    @staticmethod
+    def arrays(out) -> Dict:
+        return dict(out._arrays) if out is not None else None
+
+
+class SolverError(RuntimeError):
+    pass
+
+
+class Engine:
+    """One CUDA device, one stream, one solver context."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _abi.load_library()
+        self.device = device
+        self.ctx = self.lib.coinfer_ctx_create(device)
+        if not self.ctx:
+            raise SolverError(f"coinfer: cannot create a context on CUDA device {device}")
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.coinfer_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream) -> None:
+        """Run on a torch.cuda.Stream (or raw cudaStream_t int); None = own stream."""
+        h = None if stream is None else getattr(stream, "cuda_stream", stream)
+        self._check(self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(h) if h else None))
+
+    def synchronize(self) -> None:
+        self._check(self.lib.coinfer_ctx_synchronize(self.ctx))
+
+    def fp64_peak(self) -> float:
+        """Measured fp64-pipe throughput of this GPU (instructions x lanes / s)."""
+        v = C.c_double()
+        self._check(self.lib.coinfer_probe_fp64(self.ctx, C.byref(v)))
+        return v.value
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.coinfer_ctx_launch_count(self.ctx))
+
+    def _check(self, rc: int) -> None:
+        if rc != _abi.OK:
+            msg = self.lib.coinfer_last_error(self.ctx).decode()
+            if rc in (_abi.E_ARG, _abi.E_PROFILE):
+                raise ValueError(msg)
+            raise SolverError(f"coinfer error {rc}: {msg}")
+
+    def _mem(self, users) -> int:
+        if _is_torch(users["deadline"]):
+            # device batches run on torch's current stream, so tensor lifetimes,
+            # ordering and torch.cuda.Event timing all follow torch's stream
+            s = torch.cuda.current_stream(self.device)
+            self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(s.cuda_stream))
+            return _abi.MEM_DEVICE
+        self.lib.coinfer_ctx_set_stream(self.ctx, None)
+        return _abi.MEM_HOST
+
+    def _aux(self, x, mem, dtype):
+        if x is None:
+            return None
+        if mem == _abi.MEM_DEVICE:
+            return x.contiguous() if _is_torch(x) else torch.as_tensor(
+                np.asarray(x), device=f"cuda:{self.device}")
+        return np.ascontiguousarray(x, dtype=dtype)
+
+    def ipssa(self, profile, users: Dict, deadline=None, fields=None):
+        """IP-SSA for every instance (ip_ssa, offline_solvers.hpp:219-224)."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, True, False, f"cuda:{self.device}", ip_fields=fields)
+        d = self._aux(deadline, mem, np.float64)
+        self._check(self.lib.coinfer_ipssa_batch(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                 _ptr(d, C.c_double), C.byref(pk.out_ip)))
+        return Packed.arrays(pk.out_ip)
+
+    def fixed(self, profile, users: Dict, b, deadline=None, fields=None):
+        """Alg. 1 at bound b (fixed_batch_schedule, offline_solvers.hpp:208-214)."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, True, False, f"cuda:{self.device}", ip_fields=fields)
+        d = self._aux(deadline, mem, np.float64)
+        bb = self._aux(b, mem, np.int32)
+        self._check(self.lib.coinfer_fixed_batch(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                 _ptr(d, C.c_double), _ptr(bb, C.c_int32),
+                                                 C.byref(pk.out_ip)))
+        return Packed.arrays(pk.out_ip)
+
+    def og(self, profile, users: Dict, fields=None):
+        """OG optimal grouping for every instance (og, offline_solvers.hpp:286-388)."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, False, True, f"cuda:{self.device}", og_fields=fields)
+        self._check(self.lib.coinfer_og_batch(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                              C.byref(pk.out_og)))
+        return Packed.arrays(pk.out_og)
+
+    def sweep(self, profile, users: Dict, ipssa=True, og=True, ip_fields=None, og_fields=None,
+              pinned=False):
+        """IP-SSA at the smallest deadline and OG, fused, for every instance."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, ipssa, og, f"cuda:{self.device}", ip_fields=ip_fields,
+                    og_fields=og_fields, pinned=pinned)
+        self._check(self.lib.coinfer_sweep_batch(
+            self.ctx, C.byref(pk.profile), C.byref(pk.users),
+            C.byref(pk.out_ip) if ipssa else None, C.byref(pk.out_og) if og else None))
+        return Packed.arrays(pk.out_ip), Packed.arrays(pk.out_og)

@@ -1,0 +1,251 @@
+"""Test-side access to the CPU checkers (oracle/), never used by the product.
+
+  oracle()  -> oracle/liboracle.so         plain-C restatement (always buildable)
+  ref()     -> oracle/_ref/libcoinfer_ref.so  the unmodified reference headers
+               (built in the dev container from /root/reference; None if absent)
+
+Both export the product ABI's SoA entry points, so the same Packed structs
+drive them and the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2206_06304_b200 import _abi
+from paper_2206_06304_b200.engine import Packed
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libcoinfer_ref.so")
+
+_P, _U = C.POINTER(_abi.Profile), C.POINTER(_abi.Users)
+_IO, _OO = C.POINTER(_abi.IpssaOut), C.POINTER(_abi.OgOut)
+_dp, _i32p = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+
+ORACLE_SYMBOLS = {
+    "oracle_ipssa_batch": (C.c_int, [_P, _U, _dp, _IO]),
+    "oracle_fixed_batch": (C.c_int, [_P, _U, _dp, _i32p, _IO]),
+    "oracle_og_batch": (C.c_int, [_P, _U, _OO, C.c_int]),
+    "oracle_og_gtable": (C.c_int, [_P, _U, C.c_int64, C.c_int, _dp, _i32p]),
+}
+
+REF_SYMBOLS = {
+    "ref_ipssa_batch": (C.c_int, [_P, _U, _dp, _IO]),
+    "ref_fixed_batch": (C.c_int, [_P, _U, _dp, _i32p, _IO]),
+    "ref_og_batch": (C.c_int, [_P, _U, _OO]),
+    "ref_oracle_grouping_contiguous": (C.c_double, [_P, _U, C.c_int64, _i32p]),
+    "ref_oracle_grouping": (C.c_double, [_P, _U, C.c_int64, _i32p]),
+    "ref_sweep_threads": (C.c_double, [_P, _U, C.POINTER(C.c_int64), C.c_int64, C.c_int, C.c_int,
+                                       C.c_int, _dp, _dp]),
+    "ref_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "ref_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ref_rng_new": (C.c_void_p, [C.c_uint64]),
+    "ref_rng_free": (None, [C.c_void_p]),
+    "ref_rng_next": (C.c_uint64, [C.c_void_p]),
+    "ref_uniform_int": (C.c_uint64, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    "ref_uniform_real": (C.c_double, [C.c_void_p, C.c_double, C.c_double]),
+    "ref_random_scenario": (None, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double]
+                            + [_dp] * 10),
+    "ref_profile": (None, [C.c_int, C.c_int, _dp, _dp, _dp]),
+    "ref_sample_scenario": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                      C.c_uint64] + [_dp] * 9),
+    "ref_online_episode": (C.c_int, [_P, _U, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
+                                     C.c_double, C.c_uint64, C.c_int, C.c_int64, _dp,
+                                     C.POINTER(C.c_int64), _dp, _dp, _i32p, _dp]),
+}
+
+_oracle = None
+_ref = None
+
+
+def oracle():
+    global _oracle
+    if _oracle is None:
+        if not os.path.exists(ORACLE_SO):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"),
+                            os.path.join(ROOT, "oracle", "liboracle.so")], check=True)
+        _oracle = _abi.bind(C.CDLL(ORACLE_SO), ORACLE_SYMBOLS)
+    return _oracle
+
+
+def ref():
+    global _ref
+    if _ref is None and os.path.exists(REF_SO):
+        _ref = _abi.bind(C.CDLL(REF_SO), REF_SYMBOLS)
+    return _ref
+
+
+def _call_ip(fn, profile, users, deadline=None, b=None):
+    pk = Packed(profile, users, _abi.MEM_HOST, True, False)
+    d = None if deadline is None else np.ascontiguousarray(deadline, dtype=np.float64)
+    dp = d.ctypes.data_as(_dp) if d is not None else None
+    if b is None:
+        rc = fn(C.byref(pk.profile), C.byref(pk.users), dp, C.byref(pk.out_ip))
+    else:
+        bb = np.ascontiguousarray(b, dtype=np.int32)
+        rc = fn(C.byref(pk.profile), C.byref(pk.users), dp, bb.ctypes.data_as(_i32p),
+                C.byref(pk.out_ip))
+    assert rc == 0, rc
+    return Packed.arrays(pk.out_ip)
+
+
+def oracle_ipssa(profile, users, deadline=None):
+    return _call_ip(oracle().oracle_ipssa_batch, profile, users, deadline)
+
+
+def oracle_fixed(profile, users, b, deadline=None):
+    return _call_ip(oracle().oracle_fixed_batch, profile, users, deadline, b)
+
+
+def oracle_og(profile, users, fast=True):
+    pk = Packed(profile, users, _abi.MEM_HOST, False, True)
+    assert oracle().oracle_og_batch(C.byref(pk.profile), C.byref(pk.users), C.byref(pk.out_og),
+                                    1 if fast else 0) == 0
+    return Packed.arrays(pk.out_og)
+
+
+def ref_ipssa(profile, users, deadline=None):
+    return _call_ip(ref().ref_ipssa_batch, profile, users, deadline)
+
+
+def ref_fixed(profile, users, b, deadline=None):
+    return _call_ip(ref().ref_fixed_batch, profile, users, deadline, b)
+
+
+def ref_og(profile, users):
+    pk = Packed(profile, users, _abi.MEM_HOST, False, True)
+    assert ref().ref_og_batch(C.byref(pk.profile), C.byref(pk.users), C.byref(pk.out_og)) == 0
+    return Packed.arrays(pk.out_og)
+
+
+# --------------------------------------------------------------- comparison
+
+IP_KEYS = ["status", "batch_bound", "pipeline_feasible", "energy", "split", "freq",
+           "user_energy", "batch_size"]
+OG_KEYS = ["status", "fallback", "energy", "n_groups", "order", "group_of_user", "split", "freq",
+           "user_energy", "group_lo", "group_size", "group_b", "group_deadline", "group_energy",
+           "group_batch_size"]
+
+
+def _to_np(x):
+    if hasattr(x, "cpu"):
+        return x.cpu().numpy()
+    return np.asarray(x)
+
+
+def mask_valid(out: dict, kind: str, M: int):
+    """Entries that are defined (status OK; groups below n_groups)."""
+    st = _to_np(out["status"])
+    ok = st == 0
+    return ok
+
+
+def assert_same_ip(a: dict, b: dict, exact_energy=True, rtol=1e-9, where=""):
+    a = {k: _to_np(v) for k, v in a.items()}
+    b = {k: _to_np(v) for k, v in b.items()}
+    np.testing.assert_array_equal(a["status"], b["status"], err_msg=f"status {where}")
+    ok = a["status"] == 0
+    for k in ["batch_bound", "pipeline_feasible", "split", "batch_size"]:
+        if k in a and k in b:
+            np.testing.assert_array_equal(a[k][ok], b[k][ok], err_msg=f"{k} {where}")
+    for k in ["energy", "freq", "user_energy"]:
+        if k in a and k in b:
+            if exact_energy:
+                np.testing.assert_array_equal(a[k][ok], b[k][ok], err_msg=f"{k} {where}")
+            else:
+                np.testing.assert_allclose(a[k][ok], b[k][ok], rtol=rtol, atol=0,
+                                           err_msg=f"{k} {where}")
+
+
+def assert_same_og(a: dict, b: dict, exact_energy=True, rtol=1e-9, where=""):
+    a = {k: _to_np(v) for k, v in a.items()}
+    b = {k: _to_np(v) for k, v in b.items()}
+    np.testing.assert_array_equal(a["status"], b["status"], err_msg=f"status {where}")
+    ok = a["status"] == 0
+    for k in ["fallback", "n_groups", "order", "group_of_user", "split"]:
+        if k in a and k in b:
+            np.testing.assert_array_equal(a[k][ok], b[k][ok], err_msg=f"{k} {where}")
+    for k in ["energy", "freq", "user_energy"]:
+        if k in a and k in b:
+            if exact_energy:
+                np.testing.assert_array_equal(a[k][ok], b[k][ok], err_msg=f"{k} {where}")
+            else:
+                np.testing.assert_allclose(a[k][ok], b[k][ok], rtol=rtol, atol=0,
+                                           err_msg=f"{k} {where}")
+    # per-group arrays: only the first n_groups entries are defined
+    ng = a["n_groups"]
+    for idx in np.nonzero(ok)[0]:
+        g = int(ng[idx])
+        for k in ["group_lo", "group_size", "group_b", "group_batch_size"]:
+            if k in a and k in b:
+                np.testing.assert_array_equal(a[k][idx][:g], b[k][idx][:g],
+                                              err_msg=f"{k} inst {idx} {where}")
+        for k in ["group_deadline", "group_energy"]:
+            if k in a and k in b:
+                if exact_energy:
+                    np.testing.assert_array_equal(a[k][idx][:g], b[k][idx][:g],
+                                                  err_msg=f"{k} inst {idx} {where}")
+                else:
+                    np.testing.assert_allclose(a[k][idx][:g], b[k][idx][:g], rtol=rtol,
+                                               err_msg=f"{k} inst {idx} {where}")
+
+
+# ------------------------------------------------------------ instance makers
+
+def two_stage(users=1, b_max=8):
+    """testutil::two_stage (tests/helpers.hpp:17-38) as one-instance SoA."""
+    from paper_2206_06304_b200.engine import ProfileArrays
+    prof = ProfileArrays(np.array([0.01, 0.01]), np.array([1e6, 2e4, 0.0]),
+                         np.full((2, b_max), 0.01))
+    one = np.ones((1, users))
+    u = dict(f_min=0 * one, f_max=one * 1.0, kappa=one * 300.0, rate_up=one * 1e6,
+             rate_down=one * 1e6, power_up=one * 1.0, power_down=one * 1.0, arrival=0 * one,
+             deadline=one * 0.1)
+    return prof, u
+
+
+def ref_random_scenario(rng_handle, users, subtasks, growth_max, equal, margin_max=3.0):
+    """testutil::random_scenario through the reference (needs oracle/_ref)."""
+    from paper_2206_06304_b200.engine import ProfileArrays
+    r = ref()
+    bmax = users + 2
+    work = np.zeros(subtasks)
+    bits = np.zeros(subtasks + 1)
+    lat = np.zeros(subtasks * bmax)
+    arrs = [np.zeros((1, users)) for _ in range(7)]
+    r.ref_random_scenario(rng_handle, users, subtasks, growth_max, 1 if equal else 0, margin_max,
+                          *[a.ctypes.data_as(_dp) for a in [work, bits, lat] + arrs])
+    prof = ProfileArrays(work, bits, lat.reshape(subtasks, bmax))
+    names = ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline"]
+    u = dict(zip(names, arrs))
+    u["rate_down"] = u["rate_up"].copy()
+    u["power_down"] = u["power_up"].copy()
+    return prof, u
+
+
+def ref_sample_scenarios(n_inst, M, low, high, seeds, heavy=True, bandwidth=1e6):
+    """sample_scenario + profile_heavy/light through the reference, one seed per instance."""
+    from paper_2206_06304_b200.engine import ProfileArrays
+    r = ref()
+    work, bits, lat = np.zeros(4), np.zeros(5), np.zeros(4 * M)
+    r.ref_profile(1 if heavy else 0, M, work.ctypes.data_as(_dp), bits.ctypes.data_as(_dp),
+                  lat.ctypes.data_as(_dp))
+    prof = ProfileArrays(work, bits, lat.reshape(4, M))
+    names = ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline",
+             "rate_down", "power_down"]
+    u = {n: np.zeros((n_inst, M)) for n in names}
+    for k in range(n_inst):
+        row = [np.zeros(M) for _ in names]
+        assert r.ref_sample_scenario(1 if heavy else 0, M, low, high, bandwidth, int(seeds[k]),
+                                     *[a.ctypes.data_as(_dp) for a in row]) == 0
+        for n, a in zip(names, row):
+            u[n][k] = a
+    return prof, u
+
+
+def slice_users(u, k0, k1):
+    return {n: v[k0:k1] for n, v in u.items()}
