@@ -147,9 +147,11 @@ int coinfer_abi_version(void);
 /* Context: one CUDA device, one stream, a workspace.  NULL on failure. */
 coinfer_ctx* coinfer_ctx_create(int device);
 void coinfer_ctx_destroy(coinfer_ctx* ctx);
-/* Use an existing cudaStream_t (passed as void*) instead of the private one;
-   NULL restores the private stream. */
+/* Enqueue on an existing cudaStream_t (passed as void*; NULL is the legacy
+   default stream, as in CUDA) instead of the context's private stream. */
 int coinfer_ctx_set_stream(coinfer_ctx* ctx, void* stream);
+/* Go back to the context's private stream. */
+int coinfer_ctx_reset_stream(coinfer_ctx* ctx);
 int coinfer_ctx_synchronize(coinfer_ctx* ctx);
 /* Message of the last call-level error on this context ("" if none). */
 const char* coinfer_last_error(const coinfer_ctx* ctx);

@@ -72,6 +72,7 @@ PRODUCT_SYMBOLS = {
     "coinfer_ctx_create": (C.c_void_p, [C.c_int]),
     "coinfer_ctx_destroy": (None, [C.c_void_p]),
     "coinfer_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "coinfer_ctx_reset_stream": (C.c_int, [C.c_void_p]),
     "coinfer_ctx_synchronize": (C.c_int, [C.c_void_p]),
     "coinfer_last_error": (C.c_char_p, [C.c_void_p]),
     "coinfer_status_message": (C.c_char_p, [C.c_int32, C.c_char_p]),

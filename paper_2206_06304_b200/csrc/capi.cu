@@ -364,7 +364,13 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
 
 int coinfer_ctx_set_stream(coinfer_ctx* ctx, void* stream) {
   if (!ctx) return COINFER_E_ARG;
-  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return COINFER_OK;
+}
+
+int coinfer_ctx_reset_stream(coinfer_ctx* ctx) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->stream = ctx->own;
   return COINFER_OK;
 }
 

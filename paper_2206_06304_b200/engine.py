@@ -159,8 +159,11 @@ class Engine:
 
     def set_stream(self, stream) -> None:
         """Run on a torch.cuda.Stream (or raw cudaStream_t int); None = own stream."""
-        h = None if stream is None else getattr(stream, "cuda_stream", stream)
-        self._check(self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(h) if h else None))
+        if stream is None:
+            self._check(self.lib.coinfer_ctx_reset_stream(self.ctx))
+            return
+        h = getattr(stream, "cuda_stream", stream)
+        self._check(self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(h)))
 
     def synchronize(self) -> None:
         self._check(self.lib.coinfer_ctx_synchronize(self.ctx))
@@ -189,7 +192,7 @@ class Engine:
             s = torch.cuda.current_stream(self.device)
             self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(s.cuda_stream))
             return _abi.MEM_DEVICE
-        self.lib.coinfer_ctx_set_stream(self.ctx, None)
+        self.lib.coinfer_ctx_reset_stream(self.ctx)
         return _abi.MEM_HOST
 
     def _aux(self, x, mem, dtype):
