@@ -49,16 +49,19 @@ __device__ __forceinline__ int tri_idx(int i, int j, int M) {
 struct Layout {
   // byte offsets
   int rec, tri, dls, sumlat, headE, fsc;
-  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, misc;
+  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, tpre, misc;
   int headb, bstar, parent, spsc;
   int total;
 };
+
+// upper bound on warp tasks: chains <= M (IP-SSA) + M(M+1)/2 (OG rows)
+__host__ __device__ inline int max_tasks(int M) { return (M + M * (M + 1) / 2 + 31) / 32 + 1; }
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline Layout make_layout(int M, int N, int W) {
   Layout L;
-  const int REC = 4 * N + 5;
+  const int REC = rec_size(N);
   const int T = M * (M + 1) / 2;
   int o = 0;
   L.rec = o;     o = align16(o + 8 * M * REC);
@@ -76,8 +79,9 @@ __host__ __device__ inline Layout make_layout(int M, int N, int W) {
   L.ghi = o;     o = align16(o + 4 * M);
   L.headq = o;   o = align16(o + 4 * W);
   L.headlen = o; o = align16(o + 4 * W);
+  L.tpre = o;    o = align16(o + 4 * (max_tasks(M) + 1));
   L.misc = o;    o = align16(o + 4 * 16 + 8 * 4);
-  L.headb = o;   o = align16(o + 2 * W * M);
+  L.headb = o;   o = align16(o + W * M);
   L.bstar = o;   o = align16(o + T);
   L.parent = o;  o = align16(o + T);
   L.spsc = o;    o = align16(o + M);
@@ -93,7 +97,7 @@ enum { MI_STATUS = 0, MI_IPB = 1, MI_BESTI = 2, MI_NG = 3, MI_OGST = 4, MI_Q = 5
 int small_smem_bytes(int M, int N, int W) { return make_layout(M, N, W).total; }
 
 template <int N>
-__global__ void __launch_bounds__(256) solve_small_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
   using R = Rec<N>;
   constexpr int REC = R::SIZE;
   extern __shared__ __align__(16) unsigned char sm[];
@@ -115,9 +119,10 @@ __global__ void __launch_bounds__(256) solve_small_kernel(SmallArgs a) {
   int* ghi = reinterpret_cast<int*>(sm + L.ghi);
   int* headq = reinterpret_cast<int*>(sm + L.headq);
   int* headlen = reinterpret_cast<int*>(sm + L.headlen);
+  int* tpre = reinterpret_cast<int*>(sm + L.tpre);
   int* misc = reinterpret_cast<int*>(sm + L.misc);
   double* miscd = reinterpret_cast<double*>(sm + L.misc + 64);
-  int16_t* headb = reinterpret_cast<int16_t*>(sm + L.headb);
+  uint8_t* headb = reinterpret_cast<uint8_t*>(sm + L.headb);
   uint8_t* bstar = reinterpret_cast<uint8_t*>(sm + L.bstar);
   uint8_t* parent = reinterpret_cast<uint8_t*>(sm + L.parent);
   uint8_t* spsc = reinterpret_cast<uint8_t*>(sm + L.spsc);
@@ -218,18 +223,67 @@ __global__ void __launch_bounds__(256) solve_small_kernel(SmallArgs a) {
     __syncthreads();
 
     // ------------------------------------------------- phase 2: G table rows
+    // Warp tasks = 32 consecutive chains of the flat list.  Each warp owns a
+    // contiguous range of tasks balanced by step count, so a row split
+    // between two tasks of the same warp is merged in place (in b order);
+    // only the row a warp inherits from the previous warp's range goes to
+    // that warp's head buffer, merged after the single barrier below.
     const int C = rowoff[Q];
     const int ntask = (C + 31) >> 5;
-    const int rounds = (ntask + W - 1) / W;
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int t = rd * W + warp;
-      if (lane == 0) headlen[warp] = 0;
-      if (t < ntask) {
+    for (int t = tid; t < ntask; t += NT) {
+      const int c = t * 32;
+      int lo = 0, hi = Q - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rowoff[mid] <= c) lo = mid; else hi = mid - 1;
+      }
+      tpre[t + 1] = (lo < nip ? M : M - (lo - nip)) + 4;  // steps + setup
+    }
+    __syncthreads();
+    if (tid == 0) {
+      tpre[0] = 0;
+      for (int t = 0; t < ntask; ++t) tpre[t + 1] += tpre[t];
+    }
+    __syncthreads();
+    {
+      // this warp's task range [t0, t1): balanced prefix cut
+      const int total_cost = tpre[ntask];
+      auto cut = [&](int w) {
+        const int target = (int)(((long long)total_cost * w) / W);
+        int lo = 0, hi = ntask;  // first t with tpre[t] >= target
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tpre[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+      };
+      const int t0 = cut(warp), t1 = cut(warp + 1);
+      const int c0 = t0 * 32;  // first chain of this warp's range
+      // head buffer: the row (if any) that started in an earlier warp's range
+      int hq = -1, hlen = 0;
+      if (t0 < t1) {
+        int lo = 0, hi = Q - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (rowoff[mid] <= c0) lo = mid; else hi = mid - 1;
+        }
+        if (rowoff[lo] < c0) {
+          hq = lo;
+          hlen = lo < nip ? M : M - (lo - nip);
+        }
+      }
+      for (int kk = lane; kk < hlen; kk += 32) headE[warp * M + kk] = INF;
+      if (lane == 0) {
+        headq[warp] = hq;
+        headlen[warp] = hlen;
+      }
+      __syncwarp();
+      const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
+      for (int t = t0; t < t1; ++t) {
         const int c = t * 32 + lane;
         const bool has = c < C;
-        // segment (row) of this lane: largest q with rowoff[q] <= c
-        int lo = 0, hi = Q - 1;
         const int cc = has ? c : C - 1;
+        int lo = 0, hi = Q - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (rowoff[mid] <= cc) lo = mid; else hi = mid - 1;
@@ -237,115 +291,104 @@ __global__ void __launch_bounds__(256) solve_small_kernel(SmallArgs a) {
         const int q = lo;
         const bool isip = q < nip;
         const int row = q - nip;
-        const int qlo = rowoff[q], qhi = rowoff[q + 1];
+        const int qlo = rowoff[q];
         const int b0q = b0s[q];
         const int bidx = cc - qlo + 1;
         const bool allocal = bidx == b0q;
         const int len = isip ? M : M - row;
-        const double d = isip ? l_ip : dls[row];
+        const bool to_head = qlo < c0;  // row inherited from the previous range
         double s[N];
-        if (!allocal) start_times<N>(a.lat, P.bmax, d, bidx, s);
-        else
+        if (!allocal) {
+          start_times<N>(a.lat, P.bmax, isip ? l_ip : dls[row], bidx, s);
+        } else {
 #pragma unroll
-          for (int n = 0; n < N; ++n) s[n] = 0.0;
-        const int seg_start = max(qlo - t * 32, 0);
-        const int seg_end = min(qhi - t * 32, 32);
-        const bool cont = qlo < t * 32;  // only the lane-0 segment can continue
-        const unsigned segmask =
-            (seg_end >= 32 ? kFull : ((1u << seg_end) - 1u)) & ~((1u << seg_start) - 1u);
+          for (int n = 0; n < N; ++n) s[n] = -INF;
+        }
         const int steps = __shfl_sync(kFull, len, 0);
+        const int q_first = __shfl_sync(kFull, q, 0);
+        const int q_last = __shfl_sync(kFull, q, 31);
         bool alive = has;
         double total = 0.0;
         int offl = 0;
         for (int kk = 0; kk < steps; ++kk) {
           if (alive && kk < len) {
             const int ri = isip ? rank[kk] : row + kk;
-            const double* r = rec + ri * REC;
-            int sp;
-            double f;
-            choose<N>(r, P, s, !allocal, sp, f);
-            if (sp < 0) {
-              alive = false;
-            } else {
-              total = fold<N>(r, sp, f, total);
-              offl += sp < N;
-            }
+            const int sp = eval_fold<N>(rec_s + (uint32_t)(ri * REC * 8), P, s, allocal, total);
+            alive = sp >= 0;
+            offl += (sp >= 0 && sp < N);
           }
           const int size = kk + 1;
           const bool cand = alive && kk < len && (!isip || kk == M - 1) &&
                             (allocal ? (size >= b0q) : (bidx <= size && offl <= bidx));
-          const unsigned bal = __ballot_sync(kFull, cand);
-          double res = INF;
-          int resb = 0;
-          if (bal) {
-            const double e = cand ? total : INF;
-            double mn = e;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-              const double o = __shfl_down_sync(kFull, mn, off);
-              if (lane + off < seg_end && o < mn) mn = o;
-            }
-            const double mh = __shfl_sync(kFull, mn, seg_start);
-            const unsigned wm = __ballot_sync(kFull, cand && e == mh) & segmask;
-            if (wm) {
-              const int win = 31 - __clz(wm);
-              int wb = t * 32 + win - qlo + 1;
-              if (wb == b0q) wb = size;  // all-local chain: largest admissible b
-              res = mh;
-              resb = wb;
-            }
-          }
-          if (lane == seg_start && kk < len) {
-            if (cont) {
-              headE[warp * M + kk] = res;
-              headb[warp * M + kk] = (int16_t)resb;
-            } else if (res != INF) {
-              if (isip) {
-                miscd[0] = res;
-                misc[MI_IPB] = resb;
-              } else {
-                const int x = tri_idx(row, row + kk, M);
-                tri[x] = res;
-                bstar[x] = (uint8_t)resb;
+          if (__any_sync(kFull, cand)) {
+            // segmented lexicographic argmin (energy asc, b desc) with
+            // redux.sync over the 64-bit energy bits (energies are >= +0,
+            // so the unsigned bit order is the numeric order)
+            const unsigned long long key = (unsigned long long)__double_as_longlong(total);
+            const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+            for (int sq = q_first; sq <= q_last; ++sq) {
+              const bool mine = cand && q == sq;
+              const unsigned mh = __reduce_min_sync(kFull, mine ? khi : 0xffffffffu);
+              const bool hit = mine && khi == mh;
+              const unsigned ml = __reduce_min_sync(kFull, hit ? klo : 0xffffffffu);
+              const unsigned wm = __ballot_sync(kFull, hit && klo == ml);
+              if (wm != 0u && lane == 31 - __clz(wm)) {
+                const double e = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+                const int wb = allocal ? size : bidx;  // all-local chain: largest admissible b
+                double* tE;
+                uint8_t* tB;
+                if (to_head) {
+                  tE = headE + warp * M + kk;
+                  tB = headb + warp * M + kk;
+                } else if (isip) {
+                  tE = miscd;
+                  tB = nullptr;
+                } else {
+                  const int x = tri_idx(row, row + kk, M);
+                  tE = tri + x;
+                  tB = bstar + x;
+                }
+                if (e <= *tE) {  // later chains carry larger b: they win ties
+                  *tE = e;
+                  if (tB) *tB = (uint8_t)wb;
+                  else misc[MI_IPB] = wb;
+                }
               }
             }
           }
         }
-        if (cont && lane == 0) {
-          headq[warp] = q;
-          headlen[warp] = len;
-        }
+        __syncwarp();
       }
-      __syncthreads();
-      if (warp == 0) {
-        for (int w = 0; w < W; ++w) {
-          const int hl = headlen[w];
-          if (hl == 0) continue;
-          const int q = headq[w];
-          const bool isip = q < nip;
-          const int row = q - nip;
-          for (int kk = lane; kk < hl; kk += 32) {
-            const double e = headE[w * M + kk];
-            if (e == INF) continue;
-            const int hb = headb[w * M + kk];
-            if (isip) {
-              if (kk == M - 1 && e <= miscd[0]) {
-                miscd[0] = e;
-                misc[MI_IPB] = hb;
-              }
-            } else {
-              const int x = tri_idx(row, row + kk, M);
-              if (e <= tri[x]) {  // later chains carry larger b: they win ties
-                tri[x] = e;
-                bstar[x] = (uint8_t)hb;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    if (warp == 0) {
+      for (int w = 1; w < W; ++w) {
+        const int hl = headlen[w];
+        if (hl == 0) continue;
+        const int q = headq[w];
+        const bool isip = q < nip;
+        const int row = q - nip;
+        for (int kk = lane; kk < hl; kk += 32) {
+          const double e = headE[w * M + kk];
+          if (e == INF) continue;
+          const int hb = headb[w * M + kk];
+          if (isip) {
+            if (kk == M - 1 && e <= miscd[0]) {
+              miscd[0] = e;
+              misc[MI_IPB] = hb;
+            }
+          } else {
+            const int x = tri_idx(row, row + kk, M);
+            if (e <= tri[x]) {
+              tri[x] = e;
+              bstar[x] = (uint8_t)hb;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
 
     // ------------------------------------------------- phase 3: IP-SSA output
     if (a.do_ip) {
@@ -690,7 +733,7 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
   }
 }
 
-int fixed_smem_bytes(int M, int N) { return 8 * M * (4 * N + 5) + 8 * M + 4 * M + 16; }
+int fixed_smem_bytes(int M, int N) { return 8 * M * rec_size(N) + 8 * M + 4 * M + 16; }
 
 // ------------------------------------------------------------ host launch
 template <int N>
@@ -699,6 +742,9 @@ static cudaError_t launch_small_n(const SmallArgs& a, int threads, int grid, cud
   const int smem = small_smem_bytes(a.M, N, W);
   cudaError_t e = cudaFuncSetAttribute(solve_small_kernel<N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(solve_small_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           100);
   if (e != cudaSuccess) return e;
   solve_small_kernel<N><<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
