@@ -10,8 +10,18 @@
 
 namespace cfb {
 
+// Byte offsets of the fused kernel's shared-memory regions; computed on the
+// host once per launch so the kernel reads them from the constant bank.
+struct SmemLayout {
+  int rec, tri, dls, sumlat, headE, fsc;
+  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, tpre, misc;
+  int headb, bstar, parent, spsc, ipb;
+  int total;
+};
+
 // Arguments of the per-instance kernels; all pointers are device memory.
 struct SmallArgs {
+  SmemLayout L;
   ProfileConst P;
   const double* lat;  // [N*bmax] F_n(b)
   int64_t n_inst;

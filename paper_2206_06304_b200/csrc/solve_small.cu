@@ -46,13 +46,7 @@ __device__ __forceinline__ int tri_idx(int i, int j, int M) {
   return i * M - ((i * (i - 1)) >> 1) + (j - i);
 }
 
-struct Layout {
-  // byte offsets
-  int rec, tri, dls, sumlat, headE, fsc;
-  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, tpre, misc;
-  int headb, bstar, parent, spsc;
-  int total;
-};
+using Layout = SmemLayout;
 
 // upper bound on warp tasks: chains <= M (IP-SSA) + M(M+1)/2 (OG rows)
 __host__ __device__ inline int max_tasks(int M) { return (M + M * (M + 1) / 2 + 31) / 32 + 1; }
@@ -85,6 +79,7 @@ __host__ __device__ inline Layout make_layout(int M, int N, int W) {
   L.bstar = o;   o = align16(o + T);
   L.parent = o;  o = align16(o + T);
   L.spsc = o;    o = align16(o + M);
+  L.ipb = o;     o = align16(o + 16);
   L.total = o;
   return L;
 }
@@ -103,7 +98,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int M = a.M;
   const int tid = threadIdx.x, NT = blockDim.x, W = NT >> 5, lane = tid & 31, warp = tid >> 5;
-  const Layout L = make_layout(M, N, W);
+  const Layout& L = a.L;
   double* rec = reinterpret_cast<double*>(sm + L.rec);
   double* tri = reinterpret_cast<double*>(sm + L.tri);
   double* dls = reinterpret_cast<double*>(sm + L.dls);
@@ -126,6 +121,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
   uint8_t* bstar = reinterpret_cast<uint8_t*>(sm + L.bstar);
   uint8_t* parent = reinterpret_cast<uint8_t*>(sm + L.parent);
   uint8_t* spsc = reinterpret_cast<uint8_t*>(sm + L.spsc);
+  uint8_t* ipb = reinterpret_cast<uint8_t*>(sm + L.ipb);
   const ProfileConst& P = a.P;
   const double INF = dinf();
 
@@ -218,7 +214,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       rowoff[0] = 0;
       for (int q = 0; q < Q; ++q) rowoff[q + 1] += rowoff[q];
       miscd[0] = INF;  // IP-SSA best energy
-      misc[MI_IPB] = 0;
+      ipb[0] = 0;
     }
     __syncthreads();
 
@@ -279,7 +275,9 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       }
       __syncwarp();
       const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
+      const uint32_t RECB = (uint32_t)(REC * 8);
       for (int t = t0; t < t1; ++t) {
+        // ---- per-lane chain setup (hoisted out of the step loop)
         const int c = t * 32 + lane;
         const bool has = c < C;
         const int cc = has ? c : C - 1;
@@ -296,7 +294,22 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
         const int bidx = cc - qlo + 1;
         const bool allocal = bidx == b0q;
         const int len = isip ? M : M - row;
-        const bool to_head = qlo < c0;  // row inherited from the previous range
+        // candidate window: group sizes kk+1 >= b (all-local: >= b0), IP only at the end
+        const int kmin = isip ? M - 1 : (allocal ? b0q - 1 : bidx - 1);
+        // record address stride and write targets (E, b) as shared addresses
+        const uint32_t rb0 = rec_s + (uint32_t)(isip ? 0 : row) * RECB;
+        uint32_t tE0, tB0;
+        if (qlo < c0) {  // row inherited from the previous warp's range: head buffer
+          tE0 = (uint32_t)__cvta_generic_to_shared(headE + warp * M);
+          tB0 = (uint32_t)__cvta_generic_to_shared(headb + warp * M);
+        } else if (isip) {
+          tE0 = (uint32_t)__cvta_generic_to_shared(miscd) - 8u * (uint32_t)(M - 1);
+          tB0 = (uint32_t)__cvta_generic_to_shared(ipb) - (uint32_t)(M - 1);
+        } else {
+          const int x = tri_idx(row, row, M);
+          tE0 = (uint32_t)__cvta_generic_to_shared(tri + x);
+          tB0 = (uint32_t)__cvta_generic_to_shared(bstar + x);
+        }
         double s[N];
         if (!allocal) {
           start_times<N>(a.lat, P.bmax, isip ? l_ip : dls[row], bidx, s);
@@ -312,18 +325,17 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
         int offl = 0;
         for (int kk = 0; kk < steps; ++kk) {
           if (alive && kk < len) {
-            const int ri = isip ? rank[kk] : row + kk;
-            const int sp = eval_fold<N>(rec_s + (uint32_t)(ri * REC * 8), P, s, allocal, total);
+            const uint32_t rb = isip ? rec_s + (uint32_t)rank[kk] * RECB : rb0 + (uint32_t)kk * RECB;
+            const int sp = eval_fold<N>(rb, P, s, allocal, total);
             alive = sp >= 0;
             offl += (sp >= 0 && sp < N);
           }
-          const int size = kk + 1;
-          const bool cand = alive && kk < len && (!isip || kk == M - 1) &&
-                            (allocal ? (size >= b0q) : (bidx <= size && offl <= bidx));
+          const bool cand = alive && kk >= kmin && kk < len && offl <= bidx;
           if (__any_sync(kFull, cand)) {
             // segmented lexicographic argmin (energy asc, b desc) with
             // redux.sync over the 64-bit energy bits (energies are >= +0,
-            // so the unsigned bit order is the numeric order)
+            // so the unsigned bit order is the numeric order); lanes of a
+            // segment hold ascending b, so the highest tied lane wins
             const unsigned long long key = (unsigned long long)__double_as_longlong(total);
             const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
             for (int sq = q_first; sq <= q_last; ++sq) {
@@ -333,25 +345,14 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
               const unsigned ml = __reduce_min_sync(kFull, hit ? klo : 0xffffffffu);
               const unsigned wm = __ballot_sync(kFull, hit && klo == ml);
               if (wm != 0u && lane == 31 - __clz(wm)) {
-                const double e = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
-                const int wb = allocal ? size : bidx;  // all-local chain: largest admissible b
-                double* tE;
-                uint8_t* tB;
-                if (to_head) {
-                  tE = headE + warp * M + kk;
-                  tB = headb + warp * M + kk;
-                } else if (isip) {
-                  tE = miscd;
-                  tB = nullptr;
-                } else {
-                  const int x = tri_idx(row, row + kk, M);
-                  tE = tri + x;
-                  tB = bstar + x;
-                }
-                if (e <= *tE) {  // later chains carry larger b: they win ties
-                  *tE = e;
-                  if (tB) *tB = (uint8_t)wb;
-                  else misc[MI_IPB] = wb;
+                const double e = __longlong_as_double((long long)key);
+                const uint32_t aE = tE0 + 8u * (uint32_t)kk, aB = tB0 + (uint32_t)kk;
+                double cur;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cur) : "r"(aE) : "memory");
+                if (e <= cur) {  // later chains carry larger b: they win ties
+                  const unsigned short wb = (unsigned short)(allocal ? kk + 1 : bidx);
+                  asm volatile("st.shared.f64 [%0], %1;" ::"r"(aE), "d"(e) : "memory");
+                  asm volatile("st.shared.u8 [%0], %1;" ::"r"(aB), "h"(wb) : "memory");
                 }
               }
             }
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
           if (isip) {
             if (kk == M - 1 && e <= miscd[0]) {
               miscd[0] = e;
-              misc[MI_IPB] = hb;
+              ipb[0] = (uint8_t)hb;
             }
           } else {
             const int x = tri_idx(row, row + kk, M);
@@ -393,13 +394,13 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
     // ------------------------------------------------- phase 3: IP-SSA output
     if (a.do_ip) {
       const double ipE = miscd[0];
-      const int ipb = misc[MI_IPB];
+      const int ipbv = ipb[0];
       if (ipE == INF) {
         if (tid == 0 && a.ip.status) a.ip.status[k] = COINFER_ST_INFEASIBLE;
       } else {
-        const bool pipe = ipb < b0s[0];
+        const bool pipe = ipbv < b0s[0];
         double s[N];
-        if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipb, s);
+        if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipbv, s);
         else
 #pragma unroll
           for (int n = 0; n < N; ++n) s[n] = 0.0;
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
         }
         if (tid == 0) {
           if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
-          if (a.ip.batch_bound) a.ip.batch_bound[k] = ipb;
+          if (a.ip.batch_bound) a.ip.batch_bound[k] = ipbv;
           if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = pipe;
           if (a.ip.energy) a.ip.energy[k] = ipE;
         }
@@ -737,9 +738,11 @@ int fixed_smem_bytes(int M, int N) { return 8 * M * rec_size(N) + 8 * M + 4 * M 
 
 // ------------------------------------------------------------ host launch
 template <int N>
-static cudaError_t launch_small_n(const SmallArgs& a, int threads, int grid, cudaStream_t st) {
+static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, cudaStream_t st) {
   const int W = threads / 32;
-  const int smem = small_smem_bytes(a.M, N, W);
+  SmallArgs a = a_in;
+  a.L = make_layout(a.M, N, W);
+  const int smem = a.L.total;
   cudaError_t e = cudaFuncSetAttribute(solve_small_kernel<N>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
