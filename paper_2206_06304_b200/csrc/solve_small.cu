@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       __syncwarp();
       const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
       const uint32_t RECB = (uint32_t)(REC * 8);
+      bool num_ok = true;  // div.rn.f64 fast-path numerator test, once per launch
+#pragma unroll
+      for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(P.prefix[n]);
       for (int t = t0; t < t1; ++t) {
         // ---- per-lane chain setup (hoisted out of the step loop)
         const int c = t * 32 + lane;
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
         for (int kk = 0; kk < steps; ++kk) {
           if (alive && kk < len) {
             const uint32_t rb = isip ? rec_s + (uint32_t)rank[kk] * RECB : rb0 + (uint32_t)kk * RECB;
-            const int sp = eval_fold<N>(rb, P, s, allocal, total);
+            const int sp = eval_fold<N>(rb, P, s, allocal, num_ok, total);
             alive = sp >= 0;
             offl += (sp >= 0 && sp < N);
           }
