@@ -13,7 +13,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcoinfer_b200.so")
+LIB_PATH = os.environ.get("COINFER_LIB") or os.path.join(_HERE, "libcoinfer_b200.so")
 
 ABI_VERSION = 1
 OK, E_ARG, E_PROFILE, E_CUDA, E_UNSUPPORTED = 0, 1, 2, 3, 4

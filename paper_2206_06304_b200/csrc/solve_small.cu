@@ -39,6 +39,24 @@
 
 namespace cfb {
 
+#ifdef CFB_PHASE_TIMING
+// per-phase SM cycles summed over CTAs (timing builds only)
+__device__ unsigned long long g_phase_cycles[8];
+#define CFB_MARK(i)                                                        \
+  do {                                                                     \
+    __syncthreads();                                                       \
+    if (threadIdx.x == 0) {                                                \
+      const long long now = clock64();                                     \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(now - t_mark));   \
+      t_mark = now;                                                        \
+    }                                                                      \
+  } while (0)
+#else
+#define CFB_MARK(i) \
+  do {              \
+  } while (0)
+#endif
+
 namespace {
 
 __device__ __forceinline__ int tri_idx(int i, int j, int M) {
@@ -92,7 +110,14 @@ enum { MI_STATUS = 0, MI_IPB = 1, MI_BESTI = 2, MI_NG = 3, MI_OGST = 4, MI_Q = 5
 int small_smem_bytes(int M, int N, int W) { return make_layout(M, N, W).total; }
 
 template <int N>
-__global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
+#ifndef CFB_SMALL_MINB
+#define CFB_SMALL_MINB 3
+#endif
+#ifndef CFB_CPL
+#define CFB_CPL 1  // chains per lane in the G phase
+#endif
+__global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallArgs a) {
+  constexpr int K = CFB_CPL;
   using R = Rec<N>;
   constexpr int REC = R::SIZE;
   extern __shared__ __align__(16) unsigned char sm[];
@@ -148,6 +173,9 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       continue;
     }
 
+#ifdef CFB_PHASE_TIMING
+    long long t_mark = clock64();
+#endif
     // ------------------------------------------- phase 0: check, sort, hoist
     if (tid == 0) misc[MI_STATUS] = INT_MAX;
     __syncthreads();
@@ -200,7 +228,8 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       const double d = isip ? l_ip : dls[row];
       const int b0 = first_infeasible<N>(a.lat, P.bmax, d, len);
       b0s[q] = b0;
-      rowoff[q + 1] = b0 < len ? b0 : len;  // cnt, prefix-summed below
+      const int cnt = b0 < len ? b0 : len;  // chains of this row
+      rowoff[q + 1] = (cnt + K - 1) / K;     // lane tuples of K chains, prefix-summed below
     }
     for (int sz = tid + 1; sz <= M; sz += NT) {  // sum_latency (offline_solvers.hpp:42-47)
       double t = 0.0;
@@ -218,6 +247,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
     }
     __syncthreads();
 
+    CFB_MARK(0);
     // ------------------------------------------------- phase 2: G table rows
     // Warp tasks = 32 consecutive chains of the flat list.  Each warp owns a
     // contiguous range of tasks balanced by step count, so a row split
@@ -280,7 +310,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
 #pragma unroll
       for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(P.prefix[n]);
       for (int t = t0; t < t1; ++t) {
-        // ---- per-lane chain setup (hoisted out of the step loop)
+        // ---- per-lane setup: lane = one pair of chains (b, b+1) of one row
         const int c = t * 32 + lane;
         const bool has = c < C;
         const int cc = has ? c : C - 1;
@@ -294,12 +324,29 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
         const int row = q - nip;
         const int qlo = rowoff[q];
         const int b0q = b0s[q];
-        const int bidx = cc - qlo + 1;
-        const bool allocal = bidx == b0q;
         const int len = isip ? M : M - row;
-        // candidate window: group sizes kk+1 >= b (all-local: >= b0), IP only at the end
-        const int kmin = isip ? M - 1 : (allocal ? b0q - 1 : bidx - 1);
-        // record address stride and write targets (E, b) as shared addresses
+        const int cnt = b0q < len ? b0q : len;
+        const int b1 = K * (cc - qlo) + 1;  // first bound of this lane's K chains
+        bool al[K], alive[K];
+        int bk[K], kmin[K], off[K];
+        double s[K][N], tot[K];
+        const double dlq = isip ? l_ip : dls[row];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          bk[k] = b1 + k;
+          alive[k] = has && bk[k] <= cnt;
+          al[k] = bk[k] == b0q;
+          // candidate window: group sizes kk+1 >= b (all-local: >= b0), IP only at the end
+          kmin[k] = isip ? M - 1 : (al[k] ? b0q - 1 : bk[k] - 1);
+          off[k] = 0;
+          tot[k] = 0.0;
+          if (alive[k] && !al[k]) {
+            start_times<N>(a.lat, P.bmax, dlq, bk[k], s[k]);
+          } else {
+#pragma unroll
+            for (int n = 0; n < N; ++n) s[k][n] = -1.0;
+          }
+        }
         const uint32_t rb0 = rec_s + (uint32_t)(isip ? 0 : row) * RECB;
         uint32_t tE0, tB0;
         if (qlo < c0) {  // row inherited from the previous warp's range: head buffer
@@ -313,50 +360,66 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
           tE0 = (uint32_t)__cvta_generic_to_shared(tri + x);
           tB0 = (uint32_t)__cvta_generic_to_shared(bstar + x);
         }
-        double s[N];
-        if (!allocal) {
-          start_times<N>(a.lat, P.bmax, isip ? l_ip : dls[row], bidx, s);
-        } else {
-#pragma unroll
-          for (int n = 0; n < N; ++n) s[n] = -INF;
-        }
         const int steps = __shfl_sync(kFull, len, 0);
-        const int q_first = __shfl_sync(kFull, q, 0);
-        const int q_last = __shfl_sync(kFull, q, 31);
-        bool alive = has;
-        double total = 0.0;
-        int offl = 0;
+        const int nvalid = min(32, C - t * 32);
+        const int seg_lo = has ? max(qlo - t * 32, 0) : nvalid;
+        const int seg_hi = has ? min(rowoff[q + 1] - t * 32, nvalid) : 32;
+        const unsigned segmask =
+            (seg_hi >= 32 ? kFull : ((1u << seg_hi) - 1u)) & ~((1u << seg_lo) - 1u);
         for (int kk = 0; kk < steps; ++kk) {
-          if (alive && kk < len) {
-            const uint32_t rb = isip ? rec_s + (uint32_t)rank[kk] * RECB : rb0 + (uint32_t)kk * RECB;
-            const int sp = eval_fold<N>(rb, P, s, allocal, num_ok, total);
-            alive = sp >= 0;
-            offl += (sp >= 0 && sp < N);
+          bool live[K], any_live = false;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            live[k] = alive[k] && kk < len;
+            any_live = any_live || live[k];
           }
-          const bool cand = alive && kk >= kmin && kk < len && offl <= bidx;
+          if (any_live) {
+            const uint32_t rb = isip ? rec_s + (uint32_t)rank[kk] * RECB : rb0 + (uint32_t)kk * RECB;
+            int sp[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) sp[k] = 0;
+            eval_multi<N, K>(rb, P, s, al, num_ok, live, tot, sp);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+              if (live[k]) {
+                alive[k] = sp[k] >= 0;
+                off[k] += (sp[k] >= 0 && sp[k] < N);
+              }
+          }
+          // in-lane argmin first: a later chain (larger b) wins ties
+          bool cand = false;
+          double tbest = 0.0;
+          unsigned short wb = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const bool ck = alive[k] && kk >= kmin[k] && kk < len && off[k] <= bk[k];
+            if (ck && (!cand || tot[k] <= tbest)) {
+              tbest = tot[k];
+              wb = (unsigned short)(al[k] ? kk + 1 : bk[k]);  // all-local: largest admissible b
+            }
+            cand = cand || ck;
+          }
           if (__any_sync(kFull, cand)) {
-            // segmented lexicographic argmin (energy asc, b desc) with
-            // redux.sync over the 64-bit energy bits (energies are >= +0,
-            // so the unsigned bit order is the numeric order); lanes of a
-            // segment hold ascending b, so the highest tied lane wins
-            const unsigned long long key = (unsigned long long)__double_as_longlong(total);
+            // segmented lexicographic argmin over the lanes of each row
+            // segment with redux.sync on the 64-bit energy bits (energies are
+            // >= +0, so the unsigned bit order is the numeric order); lanes
+            // of a segment hold ascending b, so the highest tied lane wins
+            const unsigned long long key = (unsigned long long)__double_as_longlong(tbest);
             const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
-            for (int sq = q_first; sq <= q_last; ++sq) {
-              const bool mine = cand && q == sq;
-              const unsigned mh = __reduce_min_sync(kFull, mine ? khi : 0xffffffffu);
-              const bool hit = mine && khi == mh;
-              const unsigned ml = __reduce_min_sync(kFull, hit ? klo : 0xffffffffu);
-              const unsigned wm = __ballot_sync(kFull, hit && klo == ml);
-              if (wm != 0u && lane == 31 - __clz(wm)) {
-                const double e = __longlong_as_double((long long)key);
-                const uint32_t aE = tE0 + 8u * (uint32_t)kk, aB = tB0 + (uint32_t)kk;
-                double cur;
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cur) : "r"(aE) : "memory");
-                if (e <= cur) {  // later chains carry larger b: they win ties
-                  const unsigned short wb = (unsigned short)(allocal ? kk + 1 : bidx);
-                  asm volatile("st.shared.f64 [%0], %1;" ::"r"(aE), "d"(e) : "memory");
-                  asm volatile("st.shared.u8 [%0], %1;" ::"r"(aB), "h"(wb) : "memory");
-                }
+            const unsigned mh = __reduce_min_sync(segmask, cand ? khi : 0xffffffffu);
+            const bool hit = cand && khi == mh;
+            unsigned wm = __ballot_sync(kFull, hit) & segmask;
+            if (__any_sync(kFull, __popc(wm) > 1)) {  // a tie in the high word: low word decides
+              const unsigned ml = __reduce_min_sync(segmask, hit ? klo : 0xffffffffu);
+              wm = __ballot_sync(kFull, hit && klo == ml) & segmask;
+            }
+            if (wm != 0u && lane == 31 - __clz(wm)) {
+              const uint32_t aE = tE0 + 8u * (uint32_t)kk, aB = tB0 + (uint32_t)kk;
+              double cur;
+              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cur) : "r"(aE) : "memory");
+              if (tbest <= cur) {  // later chains carry larger b: they win ties
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"(aE), "d"(tbest) : "memory");
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(aB), "h"(wb) : "memory");
               }
             }
           }
@@ -394,6 +457,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
     }
     __syncthreads();
 
+    CFB_MARK(1);
     // ------------------------------------------------- phase 3: IP-SSA output
     if (a.do_ip) {
       const double ipE = miscd[0];
@@ -436,41 +500,45 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
     }
     if (!a.do_og) continue;
 
+    CFB_MARK(2);
     // ---------------------------------------------------- phase 4: OG DP
-    // S[0][j] = G[0][j] already in place.
+    // S[i][j] = min over feasible prev < i of S[prev][i-1] + G[i][j], strict
+    // '<' so the smallest prev wins ties (offline_solvers.hpp:313-330); in
+    // place over the triangle (S[0][j] = G[0][j] already).  Stage i: Qp
+    // threads per cell j split the prevs (strided), each keeps a running
+    // lexicographic (value, prev) minimum, and the Qp partials combine by the
+    // same order, which equals the reference's ascending scan.  groups_fit is
+    // monotone in prev (sorted deadlines), so a thread stops at its first
+    // infeasible prev.
     for (int i = 1; i < M; ++i) {
       const int nj = M - i;
-      int Qp = 1;  // threads per j, power of two <= 32
+      int Qp = 1;  // threads per cell, a power of two <= 32
       while (Qp < 32 && nj * Qp * 2 <= NT && Qp < i) Qp <<= 1;
       const int pairs = nj * Qp;
-      const int iters = (pairs + NT - 1) / NT;
       const double di = dls[i];
-      for (int it = 0; it < iters; ++it) {
-        const int t = it * NT + tid;
+      const int col = tri_idx(0, i - 1, M);  // S[0][i-1]; S[p][i-1] = col + p*(M-1) - p(p-1)/2
+      for (int t0 = 0; t0 < pairs; t0 += NT) {
+        const int t = t0 + tid;
         const bool act = t < pairs;
         const int j = i + (act ? t / Qp : 0);
-        const int qq = t % Qp;
+        const int qq = t & (Qp - 1);
         double best = INF;
         int bp = 255;
-        double g = INF;
         if (act) {
-          g = tri[tri_idx(i, j, M)];
+          const double g = tri[tri_idx(i, j, M)];
           if (g != INF) {
             const double thr = sumlat[j - i + 1];
             for (int prev = qq; prev < i; prev += Qp) {
-              // groups_fit (offline_solvers.hpp:229-232); feasible prevs form a prefix
-              if (!(__dadd_rn(dls[prev], thr) <= di)) break;
-              const double sp = tri[tri_idx(prev, i - 1, M)];
-              if (sp == INF) continue;
+              if (!(__dadd_rn(dls[prev], thr) <= di)) break;  // groups_fit, prefix in prev
+              const double sp = tri[col + prev * (M - 1) - ((prev * (prev - 1)) >> 1)];
               const double cand = __dadd_rn(sp, g);
-              if (cand < best) {
+              if (sp != INF && cand < best) {
                 best = cand;
                 bp = prev;
               }
             }
           }
         }
-        // lexicographic (value, prev) min over the Qp threads of this j
         for (int off = 1; off < Qp; off <<= 1) {
           const double ob = __shfl_xor_sync(kFull, best, off);
           const int op = __shfl_xor_sync(kFull, bp, off);
@@ -488,6 +556,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       __syncthreads();
     }
 
+    CFB_MARK(3);
     // best_i: strict '<', smallest i (offline_solvers.hpp:332-334)
     if (warp == 0) {
       double bv = INF;
@@ -642,7 +711,7 @@ __global__ void __launch_bounds__(256, 3) solve_small_kernel(SmallArgs a) {
       if (a.og.energy) a.og.energy[k] = e;
       if (a.og.n_groups) a.og.n_groups[k] = ng;
     }
-    __syncthreads();
+    CFB_MARK(4);
   }
 }
 
@@ -786,6 +855,17 @@ static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid
     case 16: CALL(16); break;      \
     default: return cudaErrorInvalidValue; \
   }
+
+#ifdef CFB_PHASE_TIMING
+extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  }
+  return 0;
+}
+#endif
 
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st) {
 #define CFB_CALL(n) return launch_small_n<n>(a, threads, grid, st)

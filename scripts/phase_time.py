@@ -1,0 +1,19 @@
+"""Per-phase SM cycles of the fused kernel (needs a -DCFB_PHASE_TIMING build via COINFER_LIB)."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2206_06304_b200 import Engine, profile_heavy, sample_batch, _abi
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+eng = Engine(0)
+prof = profile_heavy(50)
+dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, 50, prof, seed=1).items()}
+eng.sweep(prof, dev); torch.cuda.synchronize()
+buf = (C.c_ulonglong * 8)()
+lib = _abi.load_library()
+lib.coinfer_debug_phase_cycles(buf, 1)
+eng.sweep(prof, dev); torch.cuda.synchronize()
+lib.coinfer_debug_phase_cycles(buf, 1)
+names = ["check/sort/hoist/rows", "G table", "IP-SSA out", "DP", "backtrack/stitch"]
+tot = sum(buf[:5])
+for i, n in enumerate(names):
+    print(f"{n:24s} {buf[i]/K:12.0f} cycles/instance  {buf[i]/tot*100:5.1f}%")
