@@ -33,6 +33,7 @@
 //    group is re-derived from its stored b to produce per-user outputs.
 
 #include <climits>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -111,7 +112,7 @@ int small_smem_bytes(int M, int N, int W) { return make_layout(M, N, W).total; }
 
 template <int N>
 #ifndef CFB_SMALL_MINB
-#define CFB_SMALL_MINB 3
+#define CFB_SMALL_MINB 4
 #endif
 #ifndef CFB_CPL
 #define CFB_CPL 1  // chains per lane in the G phase
@@ -187,7 +188,11 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
       if (code != COINFER_ST_OK) atomicMin(&misc[MI_STATUS], m * 32 + code);
       fsc[m] = a.dl[x];
     }
-    __syncthreads();
+    const bool simple = __syncthreads_and(M == 0 || [&] {
+      bool z = true;
+      for (int m = tid; m < M; m += NT) z = z && a.arr[base + m] == 0.0 && a.fmin[base + m] == 0.0;
+      return z;
+    }());
     int status = misc[MI_STATUS];
     if (P.bmax < M) status = COINFER_ST_SHORT_TABLE;  // checked before the users
     else if (status != INT_MAX) status &= 31;
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
         const int seg_hi = has ? min(rowoff[q + 1] - t * 32, nvalid) : 32;
         const unsigned segmask =
             (seg_hi >= 32 ? kFull : ((1u << seg_hi) - 1u)) & ~((1u << seg_lo) - 1u);
+        auto steploop = [&](auto tag) {
         for (int kk = 0; kk < steps; ++kk) {
           bool live[K], any_live = false;
 #pragma unroll
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
             int sp[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) sp[k] = 0;
-            eval_multi<N, K>(rb, P, s, al, num_ok, live, tot, sp);
+            eval_multi<N, K, decltype(tag)::value>(rb, P, s, al, num_ok, live, tot, sp);
 #pragma unroll
             for (int k = 0; k < K; ++k)
               if (live[k]) {
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
             }
             cand = cand || ck;
           }
-          if (__any_sync(kFull, cand)) {
+          {
             // segmented lexicographic argmin over the lanes of each row
             // segment with redux.sync on the 64-bit energy bits (energies are
             // >= +0, so the unsigned bit order is the numeric order); lanes
@@ -424,6 +430,11 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
             }
           }
         }
+        };
+        if (simple)
+          steploop(std::true_type{});
+        else
+          steploop(std::false_type{});
         __syncwarp();
       }
     }
