@@ -28,9 +28,11 @@ struct coinfer_ctx {
   double* d_lat = nullptr;
   size_t lat_cap = 0;
   std::vector<double> lat_host;
-  // staging workspace for host-memory calls
-  unsigned char* ws = nullptr;
-  size_t ws_cap = 0;
+  // host-memory calls: chunks alternate over two streams / two workspaces so
+  // the copies of one chunk overlap the solve of the other
+  cudaStream_t pipe[2] = {nullptr, nullptr};
+  unsigned char* ws2[2] = {nullptr, nullptr};
+  size_t ws2_cap[2] = {0, 0};
 };
 
 namespace {
@@ -85,6 +87,12 @@ int upload_latency(coinfer_ctx* ctx, const coinfer_profile* p) {
   const size_t n = (size_t)p->N * p->b_max;
   if (ctx->lat_host.size() == n && std::memcmp(ctx->lat_host.data(), p->latency, n * 8) == 0)
     return COINFER_OK;
+  if (ctx->d_lat) {
+    // a different table: kernels still in flight on any stream may read the
+    // old one, so drain the device before overwriting it (profiles change rarely)
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "synchronize before latency upload");
+  }
   if (n > ctx->lat_cap) {
     if (ctx->d_lat) cudaFree(ctx->d_lat);
     ctx->d_lat = nullptr;
@@ -146,14 +154,21 @@ void patch(unsigned char* base, T*& p) {
   if (p) p = reinterpret_cast<T*>(base + (reinterpret_cast<uintptr_t>(p) - 1));
 }
 
-int ensure_ws(coinfer_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->ws_cap) return COINFER_OK;
-  if (ctx->ws) cudaFree(ctx->ws);
-  ctx->ws = nullptr;
-  ctx->ws_cap = 0;
-  cudaError_t e = cudaMalloc(&ctx->ws, bytes);
+int ensure_ws(coinfer_ctx* ctx, int slot, size_t bytes) {
+  if (!ctx->pipe[slot]) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->pipe[slot], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate");
+  }
+  if (bytes <= ctx->ws2_cap[slot]) return COINFER_OK;
+  if (ctx->ws2[slot]) {
+    cudaStreamSynchronize(ctx->pipe[slot]);
+    cudaFree(ctx->ws2[slot]);
+  }
+  ctx->ws2[slot] = nullptr;
+  ctx->ws2_cap[slot] = 0;
+  cudaError_t e = cudaMalloc(&ctx->ws2[slot], bytes);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(workspace)");
-  ctx->ws_cap = bytes;
+  ctx->ws2_cap[slot] = bytes;
   return COINFER_OK;
 }
 
@@ -268,67 +283,122 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   if (og_in) a.og = *og_in;
   const int32_t* bdev = bvec;
 
-  const bool host = users->mem == COINFER_MEM_HOST;
-  Stager st{ctx};
-  if (host) {
-    plan_in(st, a.fmin, K * M);
-    plan_in(st, a.fmax, K * M);
-    plan_in(st, a.kappa, K * M);
-    plan_in(st, a.ru, K * M);
-    plan_in(st, a.pu, K * M);
-    plan_in(st, a.arr, K * M);
-    plan_in(st, a.dl, K * M);
-    plan_in(st, a.rd, K * M);
-    plan_in(st, a.pd, K * M);
-    plan_in(st, a.l_ip, K);
-    plan_in(st, bdev, K);
-    if (ip_in) plan_ip_out(st, a.ip, K, M, N);
-    if (og_in) plan_og_out(st, a.og, K, M, N);
-    rc = ensure_ws(ctx, st.used);
-    if (rc != COINFER_OK) return rc;
-    unsigned char* b = ctx->ws;
-    patch(b, a.fmin);
-    patch(b, a.fmax);
-    patch(b, a.kappa);
-    patch(b, a.ru);
-    patch(b, a.pu);
-    patch(b, a.arr);
-    patch(b, a.dl);
-    patch(b, a.rd);
-    patch(b, a.pd);
-    patch(b, a.l_ip);
-    patch(b, bdev);
-    if (ip_in) patch_ip_out(b, a.ip);
-    if (og_in) patch_og_out(b, a.og);
-    for (const auto& x : st.in) {
-      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, ctx->stream);
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
-    }
-  }
-
-  const int grid = (int)(K < (size_t)(1u << 30) ? K : (size_t)(1u << 30));
-  if (mode == Mode::Fixed) {
-    e = cfb::launch_fixed(a, bdev, grid, ctx->stream);
-  } else {
+  auto launch = [&](const cfb::SmallArgs& args, const int32_t* bd, size_t Kc, cudaStream_t st) {
+    const int grid = (int)(Kc < (size_t)(1u << 30) ? Kc : (size_t)(1u << 30));
+    if (mode == Mode::Fixed) return cfb::launch_fixed(args, bd, grid, st);
     // Many instances: 4 warps per CTA and several CTAs per SM.  Few
     // instances: 8 warps per CTA to spread each instance's chains wider.
-    const int threads = K >= 1024 ? 128 : 256;
-    const int smem = cfb::small_smem_bytes((int)M, (int)N, threads / 32);
-    if (smem > 227 * 1024)
-      return fail(ctx, COINFER_E_UNSUPPORTED, "instance does not fit in shared memory");
-    e = cfb::launch_small(a, threads, grid, ctx->stream);
-  }
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
-  ctx->launches += 1;
+    const int threads = Kc >= 1024 ? 128 : 256;
+    return cfb::launch_small(args, threads, grid, st);
+  };
+  if (mode != Mode::Fixed && cfb::small_smem_bytes((int)M, (int)N, 8) > 227 * 1024)
+    return fail(ctx, COINFER_E_UNSUPPORTED, "instance does not fit in shared memory");
 
-  if (host) {
+  if (users->mem == COINFER_MEM_DEVICE) {
+    e = launch(a, bdev, K, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    ctx->launches += 1;
+    return COINFER_OK;
+  }
+
+  // Host memory: chunk the batch and alternate two streams, so the H2D copy
+  // of chunk c+1 and the D2H copy of chunk c-1 overlap the solve of chunk c.
+  const size_t nch = K >= 131072 ? (K / 65536 < 8 ? K / 65536 : 8) : 1;
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t k0 = K * c / nch, k1 = K * (c + 1) / nch, Kc = k1 - k0;
+    const int slot = (int)(c & 1);
+    cfb::SmallArgs ac = a;
+    ac.n_inst = (int64_t)Kc;
+    auto off = [&](auto*& p, size_t per) {
+      if (p) p += k0 * per;
+    };
+    off(ac.fmin, M);
+    off(ac.fmax, M);
+    off(ac.kappa, M);
+    off(ac.ru, M);
+    off(ac.pu, M);
+    off(ac.arr, M);
+    off(ac.dl, M);
+    off(ac.rd, M);
+    off(ac.pd, M);
+    off(ac.l_ip, 1);
+    const int32_t* bc = bdev;
+    off(bc, 1);
+    if (ip_in) {
+      off(ac.ip.status, 1);
+      off(ac.ip.batch_bound, 1);
+      off(ac.ip.pipeline_feasible, 1);
+      off(ac.ip.energy, 1);
+      off(ac.ip.split, M);
+      off(ac.ip.freq, M);
+      off(ac.ip.user_energy, M);
+      off(ac.ip.batch_size, N);
+    }
+    if (og_in) {
+      off(ac.og.status, 1);
+      off(ac.og.fallback, 1);
+      off(ac.og.energy, 1);
+      off(ac.og.n_groups, 1);
+      off(ac.og.order, M);
+      off(ac.og.group_of_user, M);
+      off(ac.og.split, M);
+      off(ac.og.freq, M);
+      off(ac.og.user_energy, M);
+      off(ac.og.group_lo, M);
+      off(ac.og.group_size, M);
+      off(ac.og.group_b, M);
+      off(ac.og.group_deadline, M);
+      off(ac.og.group_energy, M);
+      off(ac.og.group_batch_size, M * N);
+    }
+    Stager st{ctx};
+    plan_in(st, ac.fmin, Kc * M);
+    plan_in(st, ac.fmax, Kc * M);
+    plan_in(st, ac.kappa, Kc * M);
+    plan_in(st, ac.ru, Kc * M);
+    plan_in(st, ac.pu, Kc * M);
+    plan_in(st, ac.arr, Kc * M);
+    plan_in(st, ac.dl, Kc * M);
+    plan_in(st, ac.rd, Kc * M);
+    plan_in(st, ac.pd, Kc * M);
+    plan_in(st, ac.l_ip, Kc);
+    plan_in(st, bc, Kc);
+    if (ip_in) plan_ip_out(st, ac.ip, Kc, M, N);
+    if (og_in) plan_og_out(st, ac.og, Kc, M, N);
+    rc = ensure_ws(ctx, slot, st.used);
+    if (rc != COINFER_OK) return rc;
+    unsigned char* b = ctx->ws2[slot];
+    cudaStream_t sp = ctx->pipe[slot];
+    patch(b, ac.fmin);
+    patch(b, ac.fmax);
+    patch(b, ac.kappa);
+    patch(b, ac.ru);
+    patch(b, ac.pu);
+    patch(b, ac.arr);
+    patch(b, ac.dl);
+    patch(b, ac.rd);
+    patch(b, ac.pd);
+    patch(b, ac.l_ip);
+    patch(b, bc);
+    if (ip_in) patch_ip_out(b, ac.ip);
+    if (og_in) patch_og_out(b, ac.og);
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+    }
+    e = launch(ac, bc, Kc, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    ctx->launches += 1;
     for (const auto& x : st.back) {
-      e = cudaMemcpyAsync(x.host, ctx->ws + x.off, x.bytes, cudaMemcpyDeviceToHost, ctx->stream);
+      e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
     }
-    e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "solve");
   }
+  for (int slot = 0; slot < 2; ++slot)
+    if (ctx->pipe[slot]) {
+      e = cudaStreamSynchronize(ctx->pipe[slot]);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "solve");
+    }
   return COINFER_OK;
 }
 
@@ -357,7 +427,11 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_lat) cudaFree(ctx->d_lat);
-  if (ctx->ws) cudaFree(ctx->ws);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);
+    if (ctx->ws2[i]) cudaFree(ctx->ws2[i]);
+    if (ctx->pipe[i]) cudaStreamDestroy(ctx->pipe[i]);
+  }
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }

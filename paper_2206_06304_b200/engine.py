@@ -72,6 +72,21 @@ def _kind(ctype) -> str:
             C.POINTER(C.c_uint8): "u"}[ctype]
 
 
+_PINNED = {}
+
+
+def _pinned_buffer(name, shape, dtype):
+    """Reusable page-locked staging array (allocating pinned memory per call
+    costs more than the copy).  Results in it are overwritten by the next
+    pinned call with the same output."""
+    key = (name, tuple(shape), np.dtype(dtype).str)
+    a = _PINNED.get(key)
+    if a is None:
+        a = torch.empty(shape, dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True).numpy()
+        _PINNED[key] = a
+    return a
+
+
 class Packed:
     """ctypes structs for one call plus the arrays they point into."""
 
@@ -116,8 +131,8 @@ class Packed:
                 continue
             if mem == _abi.MEM_DEVICE:
                 a = torch.empty(shapes[dim], dtype=getattr(torch, _TT[k]), device=device)
-            elif self.pinned:  # page-locked host outputs: D2H at full PCIe/C2C speed
-                a = torch.empty(shapes[dim], dtype=getattr(torch, _TT[k]), pin_memory=True).numpy()
+            elif self.pinned:  # page-locked host outputs: D2H at full PCIe speed
+                a = _pinned_buffer(name, shapes[dim], _NP[k])
             else:
                 a = np.zeros(shapes[dim], dtype=_NP[k])
             arrays[name] = a
@@ -233,7 +248,10 @@ class Engine:
 
     def sweep(self, profile, users: Dict, ipssa=True, og=True, ip_fields=None, og_fields=None,
               pinned=False):
-        """IP-SSA at the smallest deadline and OG, fused, for every instance."""
+        """IP-SSA at the smallest deadline and OG, fused, for every instance.
+
+        pinned=True (host batches): outputs land in reusable page-locked
+        buffers that the next pinned call overwrites."""
         mem = self._mem(users)
         pk = Packed(profile, users, mem, ipssa, og, f"cuda:{self.device}", ip_fields=ip_fields,
                     og_fields=og_fields, pinned=pinned)
