@@ -70,6 +70,11 @@ extern "C" {
 #define COINFER_ST_ZERO_BOUND 17    /* b == 0: "batch_start_times: b must be >= 1" (invalid_argument) */
 #define COINFER_ST_BOUND_PAST_TABLE 18 /* b > b_max: std::out_of_range "edge_batch_latency: batch size beyond table" */
 
+/* online driver (OnlineEnv, online_sim.hpp) */
+#define COINFER_ST_NOT_RELEASED 20     /* "online: users must be released at time zero" */
+#define COINFER_ST_FLOOR_ABOVE_LLOW 21 /* "online: l_low below a user's all-local floor" */
+#define COINFER_ST_SLIPPED 22          /* std::logic_error "online: task slipped below its local floor" */
+
 #define COINFER_MEM_HOST 0
 #define COINFER_MEM_DEVICE 1
 
@@ -142,6 +147,45 @@ typedef struct coinfer_og_out {
   int32_t* group_batch_size;/* [n_inst*M*N] realized batch size per sub-task per group */
 } coinfer_og_out;
 
+/* Online slot driver: run_episode(OnlineEnv(scenario, ArrivalModel, solver,
+   slot, seed), policy, horizon, seed) (online_sim.hpp:69-371), one episode
+   per seed.  Policies: the fixed TimeWindowPolicy(window, l_high) and
+   local_policy (DDPG is out of scope). */
+#define COINFER_ARRIVAL_BERNOULLI 0
+#define COINFER_ARRIVAL_IMMEDIATE 1
+#define COINFER_SOLVER_IPSSA 0
+#define COINFER_SOLVER_OG 1
+#define COINFER_POLICY_TW 0
+#define COINFER_POLICY_LOCAL 1
+
+typedef struct coinfer_online_cfg {
+  int32_t arrival;  /* COINFER_ARRIVAL_*  (ArrivalModel::kind)   */
+  int32_t solver;   /* COINFER_SOLVER_*   (OnlineSolver)         */
+  int32_t policy;   /* COINFER_POLICY_*                          */
+  int32_t window;   /* TimeWindowPolicy window, in slots          */
+  double p_arrive;  /* ArrivalModel::p_arrive                     */
+  double l_low;     /* ArrivalModel::l_low                        */
+  double l_high;    /* ArrivalModel::l_high (also the TW threshold) */
+  double slot;      /* slot length, seconds                       */
+  double threshold; /* TimeWindowPolicy threshold (the CLI uses l_high) */
+  int64_t horizon;  /* slots per episode                          */
+} coinfer_online_cfg;
+
+/* EpisodeMetrics (online_sim.hpp:274-296) per episode, plus an optional
+   per-slot trace (TraceRow reward / energy / pending_count / edge_busy) for
+   the first n_trace episodes. */
+typedef struct coinfer_online_out {
+  int32_t* status;  /* [n_ep] COINFER_ST_*                                   */
+  double* totals;   /* [n_ep*3] total_energy, total_forced_cost, total_reward */
+  int64_t* counts;  /* [n_ep*6] forced_count, solver_calls, solver_tasks,
+                       solver_groups, batches, batched_tasks                 */
+  int64_t n_trace;
+  double* trace_reward;      /* [n_trace*horizon] */
+  double* trace_energy;      /* [n_trace*horizon] */
+  int32_t* trace_pending;    /* [n_trace*horizon] */
+  double* trace_edge_busy;   /* [n_trace*horizon] */
+} coinfer_online_out;
+
 int coinfer_abi_version(void);
 
 /* Context: one CUDA device, one stream, a workspace.  NULL on failure. */
@@ -189,6 +233,15 @@ int coinfer_og_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
 int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
                         const coinfer_users* users, coinfer_ipssa_out* ipssa,
                         coinfer_og_out* og);
+
+/* Run n_ep episodes; episode e simulates scenario e % users->n_inst (each a
+   Scenario of users->M users; deadlines are only contract-checked) with
+   std::mt19937_64 seeded by seeds[e].  seeds and all outputs live in the
+   same memory kind as the users.  Config errors (ArrivalModel::check, slot,
+   horizon) return COINFER_E_ARG with the reference's message. */
+int coinfer_online_run(coinfer_ctx* ctx, const coinfer_profile* profile,
+                       const coinfer_users* scenarios, const coinfer_online_cfg* cfg,
+                       const uint64_t* seeds, int64_t n_ep, coinfer_online_out* out);
 
 #ifdef __cplusplus
 }

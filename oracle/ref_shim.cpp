@@ -374,12 +374,13 @@ int ref_sample_scenario(int heavy, int M, double lo, double hi, double bandwidth
 
 // One episode of run_episode(OnlineEnv(sample_scenario(users=M, fixed(l_high)),
 // ArrivalModel{Bernoulli, p, [l_low, l_high]}, solver, slot, seed),
-// TimeWindowPolicy(window, l_high), horizon) — the CLI's online path
+// TimeWindowPolicy(window, threshold) or local_policy (window < 0), horizon) — the CLI's online path
 // (coinfer_main.cpp:482-573).  Scenario given as SoA (one instance).
 // trace arrays (may be NULL) get per-slot reward, energy, pending, busy.
 int ref_online_episode(const coinfer_profile* p, const coinfer_users* u, int solver_og,
                        double p_arrive, int immediate, double l_low, double l_high, double slot,
-                       uint64_t seed, int window, int64_t horizon, double* totals /*[4]*/,
+                       uint64_t seed, int window, double threshold, int64_t horizon,
+                       double* totals /*[4]*/,
                        int64_t* counts /*[6]*/, double* tr_reward, double* tr_energy,
                        int32_t* tr_pending, double* tr_busy) {
   try {
@@ -390,7 +391,9 @@ int ref_online_episode(const coinfer_profile* p, const coinfer_users* u, int sol
     a.l_low = l_low;
     a.l_high = l_high;
     OnlineEnv env(sc, a, solver_og ? OnlineSolver::OG : OnlineSolver::IPSSA, slot, seed);
-    const EpisodeMetrics m = run_episode(env, TimeWindowPolicy(window, l_high), horizon, seed);
+    // window < 0 selects local_policy (online_sim.hpp:301-307)
+    const PolicyFn pol = window < 0 ? local_policy() : PolicyFn(TimeWindowPolicy(window, threshold));
+    const EpisodeMetrics m = run_episode(env, pol, horizon, seed);
     totals[0] = m.total_energy;
     totals[1] = m.total_forced_cost;
     totals[2] = m.total_reward;

@@ -66,6 +66,25 @@ class OgOut(C.Structure):
     _fields_ = [(n, t) for n, t, _ in OG_FIELDS]
 
 
+ARRIVAL_BERNOULLI, ARRIVAL_IMMEDIATE = 0, 1
+SOLVER_IPSSA, SOLVER_OG = 0, 1
+POLICY_TW, POLICY_LOCAL = 0, 1
+ST_NOT_RELEASED, ST_FLOOR_ABOVE_LLOW, ST_SLIPPED = 20, 21, 22
+
+
+class OnlineCfg(C.Structure):
+    _fields_ = [("arrival", C.c_int32), ("solver", C.c_int32), ("policy", C.c_int32),
+                ("window", C.c_int32), ("p_arrive", C.c_double), ("l_low", C.c_double),
+                ("l_high", C.c_double), ("slot", C.c_double), ("threshold", C.c_double),
+                ("horizon", C.c_int64)]
+
+
+class OnlineOut(C.Structure):
+    _fields_ = [("status", _i32p), ("totals", _dp), ("counts", _i64p), ("n_trace", C.c_int64),
+                ("trace_reward", _dp), ("trace_energy", _dp), ("trace_pending", _i32p),
+                ("trace_edge_busy", _dp)]
+
+
 # name -> (restype, argtypes) of every symbol include/coinfer_b200.h declares
 PRODUCT_SYMBOLS = {
     "coinfer_abi_version": (C.c_int, []),
@@ -86,6 +105,9 @@ PRODUCT_SYMBOLS = {
                                    C.POINTER(OgOut)]),
     "coinfer_sweep_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                       C.POINTER(IpssaOut), C.POINTER(OgOut)]),
+    "coinfer_online_run": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                     C.POINTER(OnlineCfg), C.POINTER(C.c_uint64), C.c_int64,
+                                     C.POINTER(OnlineOut)]),
 }
 
 

@@ -484,6 +484,9 @@ const char* coinfer_status_message(int32_t status, const char* solver) {
     case COINFER_ST_SHORT_TABLE: return "scenario: latency table shorter than user count";
     case COINFER_ST_ZERO_BOUND: return "batch_start_times: b must be >= 1";
     case COINFER_ST_BOUND_PAST_TABLE: return "edge_batch_latency: batch size beyond table";
+    case COINFER_ST_NOT_RELEASED: return "online: users must be released at time zero";
+    case COINFER_ST_FLOOR_ABOVE_LLOW: return "online: l_low below a user's all-local floor";
+    case COINFER_ST_SLIPPED: return "online: task slipped below its local floor";
   }
   return "unknown status";
 }
@@ -504,6 +507,160 @@ int coinfer_og_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coi
                      coinfer_og_out* out) {
   if (!out) return fail(ctx, COINFER_E_ARG, "og: null output");
   return run(ctx, profile, users, nullptr, nullptr, nullptr, out, Mode::Solve);
+}
+
+int coinfer_online_run(coinfer_ctx* ctx, const coinfer_profile* profile,
+                       const coinfer_users* sc, const coinfer_online_cfg* cfg,
+                       const uint64_t* seeds, int64_t n_ep, coinfer_online_out* out) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  if (!sc || !cfg || !out) return fail(ctx, COINFER_E_ARG, "online: null argument");
+  int rc = check_profile(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+  // ArrivalModel::check, OnlineEnv ctor, run_episode (online_sim.hpp:33-38,81,340)
+  if (cfg->l_low <= 0.0 || cfg->l_high < cfg->l_low)
+    return fail(ctx, COINFER_E_ARG, "arrivals: bad deadline range");
+  if (cfg->arrival == COINFER_ARRIVAL_BERNOULLI && (cfg->p_arrive < 0.0 || cfg->p_arrive > 1.0))
+    return fail(ctx, COINFER_E_ARG, "arrivals: p_arrive must lie in [0, 1]");
+  if (cfg->arrival != COINFER_ARRIVAL_BERNOULLI && cfg->arrival != COINFER_ARRIVAL_IMMEDIATE)
+    return fail(ctx, COINFER_E_ARG, "arrivals: unknown kind");
+  if (!(cfg->slot > 0.0)) return fail(ctx, COINFER_E_ARG, "online: slot must be positive");
+  if (cfg->horizon <= 0) return fail(ctx, COINFER_E_ARG, "run_episode: empty horizon");
+  if (cfg->solver != COINFER_SOLVER_OG && cfg->solver != COINFER_SOLVER_IPSSA)
+    return fail(ctx, COINFER_E_ARG, "online: unknown solver");
+  if (cfg->policy != COINFER_POLICY_TW && cfg->policy != COINFER_POLICY_LOCAL)
+    return fail(ctx, COINFER_E_ARG, "online: unknown policy");
+  if (sc->n_inst <= 0 || sc->M <= 0) return fail(ctx, COINFER_E_ARG, "online: need a scenario with users");
+  if (sc->M > kSmallMaxM) return fail(ctx, COINFER_E_UNSUPPORTED, "online: M above the solver limit");
+  if (n_ep <= 0) return COINFER_OK;
+  if (!seeds) return fail(ctx, COINFER_E_ARG, "online: null seeds");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  rc = upload_latency(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+
+  const size_t S = (size_t)sc->n_inst, M = (size_t)sc->M, N = (size_t)profile->N, E = (size_t)n_ep;
+  const size_t T = out->n_trace > 0 ? (size_t)out->n_trace * (size_t)cfg->horizon : 0;
+  cfb::OnlineArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.solve.P = make_const(profile);
+  a.solve.lat = ctx->d_lat;
+  a.solve.n_inst = 1;
+  a.solve.do_og = cfg->solver == COINFER_SOLVER_OG;
+  a.solve.do_ip = !a.solve.do_og;
+  a.M = sc->M;
+  a.n_scen = sc->n_inst;
+  a.fmin = sc->f_min;
+  a.fmax = sc->f_max;
+  a.kappa = sc->kappa;
+  a.ru = sc->rate_up;
+  a.pu = sc->power_up;
+  a.arr = sc->arrival;
+  a.dl = sc->deadline;
+  a.rd = sc->rate_down;
+  a.pd = sc->power_down;
+  a.immediate = cfg->arrival == COINFER_ARRIVAL_IMMEDIATE;
+  a.p_arrive = cfg->p_arrive;
+  a.l_low = cfg->l_low;
+  a.l_high = cfg->l_high;
+  a.slot = cfg->slot;
+  a.threshold = cfg->threshold;
+  a.policy = cfg->policy;
+  a.window = cfg->window;
+  a.horizon = cfg->horizon;
+  a.n_ep = n_ep;
+  a.seeds = reinterpret_cast<const unsigned long long*>(seeds);
+  a.status = out->status;
+  a.totals = out->totals;
+  a.counts = reinterpret_cast<long long*>(out->counts);
+  a.n_trace = out->n_trace;
+  a.tr_reward = out->trace_reward;
+  a.tr_energy = out->trace_energy;
+  a.tr_pending = out->trace_pending;
+  a.tr_busy = out->trace_edge_busy;
+
+  const bool host = sc->mem == COINFER_MEM_HOST;
+  Stager st{ctx};
+  if (host) {
+    plan_in(st, a.fmin, S * M);
+    plan_in(st, a.fmax, S * M);
+    plan_in(st, a.kappa, S * M);
+    plan_in(st, a.ru, S * M);
+    plan_in(st, a.pu, S * M);
+    plan_in(st, a.arr, S * M);
+    plan_in(st, a.dl, S * M);
+    plan_in(st, a.rd, S * M);
+    plan_in(st, a.pd, S * M);
+    plan_in(st, a.seeds, E);
+    plan_out(st, a.status, E);
+    plan_out(st, a.totals, 3 * E);
+    plan_out(st, a.counts, 6 * E);
+    plan_out(st, a.tr_reward, T);
+    plan_out(st, a.tr_energy, T);
+    plan_out(st, a.tr_pending, T);
+    plan_out(st, a.tr_busy, T);
+  }
+  // per-episode solver scratch, device only
+  int32_t* s_status = reinterpret_cast<int32_t*>(st.reserve(4 * E) + 1);
+  double* s_energy = reinterpret_cast<double*>(st.reserve(8 * E) + 1);
+  int32_t* s_ng = reinterpret_cast<int32_t*>(st.reserve(4 * E) + 1);
+  double* s_gdl = reinterpret_cast<double*>(st.reserve(8 * E * M) + 1);
+  int32_t* s_gbs = reinterpret_cast<int32_t*>(st.reserve(4 * E * M * N) + 1);
+  int32_t* s_ibs = reinterpret_cast<int32_t*>(st.reserve(4 * E * N) + 1);
+  rc = ensure_ws(ctx, 0, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->ws2[0];
+  cudaStream_t sp = host ? ctx->pipe[0] : ctx->stream;
+  if (host) {
+    patch(b, a.fmin);
+    patch(b, a.fmax);
+    patch(b, a.kappa);
+    patch(b, a.ru);
+    patch(b, a.pu);
+    patch(b, a.arr);
+    patch(b, a.dl);
+    patch(b, a.rd);
+    patch(b, a.pd);
+    patch(b, a.seeds);
+    patch(b, a.status);
+    patch(b, a.totals);
+    patch(b, a.counts);
+    patch(b, a.tr_reward);
+    patch(b, a.tr_energy);
+    patch(b, a.tr_pending);
+    patch(b, a.tr_busy);
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D online inputs");
+    }
+  }
+  patch(b, s_status);
+  patch(b, s_energy);
+  patch(b, s_ng);
+  patch(b, s_gdl);
+  patch(b, s_gbs);
+  patch(b, s_ibs);
+  a.solve.og.status = s_status;
+  a.solve.og.energy = s_energy;
+  a.solve.og.n_groups = s_ng;
+  a.solve.og.group_deadline = s_gdl;
+  a.solve.og.group_batch_size = s_gbs;
+  a.solve.ip.status = s_status;
+  a.solve.ip.energy = s_energy;
+  a.solve.ip.batch_size = s_ibs;
+  const int grid = (int)(E < (size_t)(1u << 30) ? E : (size_t)(1u << 30));
+  e = cfb::launch_online(a, grid, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "online kernel launch");
+  ctx->launches += 1;
+  if (host) {
+    for (const auto& x : st.back) {
+      e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H online outputs");
+    }
+    e = cudaStreamSynchronize(sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "online run");
+  }
+  return COINFER_OK;
 }
 
 int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,

@@ -33,9 +33,59 @@ struct SmallArgs {
   coinfer_og_out og;
 };
 
+// One instance's users (global or shared memory), already offset.
+struct InstIn {
+  const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl, *rd, *pd;
+  double l_ip;    // IP-SSA common deadline when has_l_ip
+  bool has_l_ip;  // else the smallest user deadline
+};
+
+// Arguments of the online driver (one warp per episode).
+struct OnlineArgs {
+  SmallArgs solve;  // profile, latency table, solver choice, per-episode scratch outputs
+  SmemLayout L;     // solver workspace for M users, one warp
+  int M;
+  int64_t n_scen;   // episode e runs scenario e % n_scen
+  const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl, *rd, *pd;
+  int immediate;
+  double p_arrive, l_low, l_high, slot, threshold;
+  int policy, window;
+  int64_t horizon, n_ep;
+  const unsigned long long* seeds;
+  int32_t* status;
+  double* totals;
+  long long* counts;
+  int64_t n_trace;
+  double *tr_reward, *tr_energy, *tr_busy;
+  int32_t* tr_pending;
+};
+
 int small_smem_bytes(int M, int N, int W);
+int online_smem_bytes(int M, int N);
+cudaError_t launch_online(const OnlineArgs& a, int grid, cudaStream_t st);
 int fixed_smem_bytes(int M, int N);
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st);
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
+
+#define CFB_DISPATCH_N(NVAL, CALL) \
+  switch (NVAL) {                  \
+    case 1: CALL(1); break;        \
+    case 2: CALL(2); break;        \
+    case 3: CALL(3); break;        \
+    case 4: CALL(4); break;        \
+    case 5: CALL(5); break;        \
+    case 6: CALL(6); break;        \
+    case 7: CALL(7); break;        \
+    case 8: CALL(8); break;        \
+    case 9: CALL(9); break;        \
+    case 10: CALL(10); break;      \
+    case 11: CALL(11); break;      \
+    case 12: CALL(12); break;      \
+    case 13: CALL(13); break;      \
+    case 14: CALL(14); break;      \
+    case 15: CALL(15); break;      \
+    case 16: CALL(16); break;      \
+    default: return cudaErrorInvalidValue; \
+  }
 
 }  // namespace cfb

@@ -32,697 +32,35 @@
 //    (j, prev) pairs split across the CTA.  Backtrack, then every chosen
 //    group is re-derived from its stored b to produce per-user outputs.
 
-#include <climits>
-#include <type_traits>
-
-#include "device_common.cuh"
-#include "kernels.h"
+#include "solve_core.cuh"
 
 namespace cfb {
 
 #ifdef CFB_PHASE_TIMING
-// per-phase SM cycles summed over CTAs (timing builds only)
 __device__ unsigned long long g_phase_cycles[8];
-#define CFB_MARK(i)                                                        \
-  do {                                                                     \
-    __syncthreads();                                                       \
-    if (threadIdx.x == 0) {                                                \
-      const long long now = clock64();                                     \
-      atomicAdd(&g_phase_cycles[i], (unsigned long long)(now - t_mark));   \
-      t_mark = now;                                                        \
-    }                                                                      \
-  } while (0)
-#else
-#define CFB_MARK(i) \
-  do {              \
-  } while (0)
 #endif
 
-namespace {
-
-__device__ __forceinline__ int tri_idx(int i, int j, int M) {
-  // row-major upper triangle incl. diagonal
-  return i * M - ((i * (i - 1)) >> 1) + (j - i);
-}
-
-using Layout = SmemLayout;
-
-// upper bound on warp tasks: chains <= M (IP-SSA) + M(M+1)/2 (OG rows)
-__host__ __device__ inline int max_tasks(int M) { return (M + M * (M + 1) / 2 + 31) / 32 + 1; }
-
-__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-
-__host__ __device__ inline Layout make_layout(int M, int N, int W) {
-  Layout L;
-  const int REC = rec_size(N);
-  const int T = M * (M + 1) / 2;
-  int o = 0;
-  L.rec = o;     o = align16(o + 8 * M * REC);
-  L.tri = o;     o = align16(o + 8 * T);
-  L.dls = o;     o = align16(o + 8 * M);
-  L.sumlat = o;  o = align16(o + 8 * (M + 1));
-  L.headE = o;   o = align16(o + 8 * W * M);
-  L.fsc = o;     o = align16(o + 8 * M);
-  L.rowoff = o;  o = align16(o + 4 * (M + 2));
-  L.b0 = o;      o = align16(o + 4 * (M + 1));
-  L.order = o;   o = align16(o + 4 * M);
-  L.rank = o;    o = align16(o + 4 * M);
-  L.gid = o;     o = align16(o + 4 * M);
-  L.glo = o;     o = align16(o + 4 * M);
-  L.ghi = o;     o = align16(o + 4 * M);
-  L.headq = o;   o = align16(o + 4 * W);
-  L.headlen = o; o = align16(o + 4 * W);
-  L.tpre = o;    o = align16(o + 4 * (max_tasks(M) + 1));
-  L.misc = o;    o = align16(o + 4 * 16 + 8 * 4);
-  L.headb = o;   o = align16(o + W * M);
-  L.bstar = o;   o = align16(o + T);
-  L.parent = o;  o = align16(o + T);
-  L.spsc = o;    o = align16(o + M);
-  L.ipb = o;     o = align16(o + 16);
-  L.total = o;
-  return L;
-}
-
-// misc slots
-enum { MI_STATUS = 0, MI_IPB = 1, MI_BESTI = 2, MI_NG = 3, MI_OGST = 4, MI_Q = 5 };
-
-}  // namespace
-
-int small_smem_bytes(int M, int N, int W) { return make_layout(M, N, W).total; }
+int small_smem_bytes(int M, int N, int W) { return small_smem_bytes_impl(M, N, W); }
 
 template <int N>
-#ifndef CFB_SMALL_MINB
-#define CFB_SMALL_MINB 4
-#endif
-#ifndef CFB_CPL
-#define CFB_CPL 1  // chains per lane in the G phase
-#endif
 __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallArgs a) {
-  constexpr int K = CFB_CPL;
-  using R = Rec<N>;
-  constexpr int REC = R::SIZE;
   extern __shared__ __align__(16) unsigned char sm[];
   const int M = a.M;
-  const int tid = threadIdx.x, NT = blockDim.x, W = NT >> 5, lane = tid & 31, warp = tid >> 5;
-  const Layout& L = a.L;
-  double* rec = reinterpret_cast<double*>(sm + L.rec);
-  double* tri = reinterpret_cast<double*>(sm + L.tri);
-  double* dls = reinterpret_cast<double*>(sm + L.dls);
-  double* sumlat = reinterpret_cast<double*>(sm + L.sumlat);
-  double* headE = reinterpret_cast<double*>(sm + L.headE);
-  double* fsc = reinterpret_cast<double*>(sm + L.fsc);
-  int* rowoff = reinterpret_cast<int*>(sm + L.rowoff);
-  int* b0s = reinterpret_cast<int*>(sm + L.b0);
-  int* order = reinterpret_cast<int*>(sm + L.order);
-  int* rank = reinterpret_cast<int*>(sm + L.rank);
-  int* gid = reinterpret_cast<int*>(sm + L.gid);
-  int* glo = reinterpret_cast<int*>(sm + L.glo);
-  int* ghi = reinterpret_cast<int*>(sm + L.ghi);
-  int* headq = reinterpret_cast<int*>(sm + L.headq);
-  int* headlen = reinterpret_cast<int*>(sm + L.headlen);
-  int* tpre = reinterpret_cast<int*>(sm + L.tpre);
-  int* misc = reinterpret_cast<int*>(sm + L.misc);
-  double* miscd = reinterpret_cast<double*>(sm + L.misc + 64);
-  uint8_t* headb = reinterpret_cast<uint8_t*>(sm + L.headb);
-  uint8_t* bstar = reinterpret_cast<uint8_t*>(sm + L.bstar);
-  uint8_t* parent = reinterpret_cast<uint8_t*>(sm + L.parent);
-  uint8_t* spsc = reinterpret_cast<uint8_t*>(sm + L.spsc);
-  uint8_t* ipb = reinterpret_cast<uint8_t*>(sm + L.ipb);
-  const ProfileConst& P = a.P;
-  const double INF = dinf();
-
   for (int64_t k = blockIdx.x; k < a.n_inst; k += gridDim.x) {
     const size_t base = (size_t)k * M;
-    // ------------------------------------------------------------------ M = 0
-    if (M == 0) {
-      if (tid == 0) {
-        if (a.do_ip) {
-          if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
-          if (a.ip.batch_bound) a.ip.batch_bound[k] = 0;
-          if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = 1;
-          if (a.ip.energy) a.ip.energy[k] = 0.0;
-          if (a.ip.batch_size)
-            for (int n = 0; n < N; ++n) a.ip.batch_size[(size_t)k * N + n] = 0;
-        }
-        if (a.do_og) {
-          if (a.og.status) a.og.status[k] = COINFER_ST_OK;
-          if (a.og.fallback) a.og.fallback[k] = 0;
-          if (a.og.energy) a.og.energy[k] = 0.0;
-          if (a.og.n_groups) a.og.n_groups[k] = 0;
-        }
-      }
-      continue;
-    }
-
-#ifdef CFB_PHASE_TIMING
-    long long t_mark = clock64();
-#endif
-    // ------------------------------------------- phase 0: check, sort, hoist
-    if (tid == 0) misc[MI_STATUS] = INT_MAX;
-    __syncthreads();
-    for (int m = tid; m < M; m += NT) {
-      const size_t x = base + m;
-      const double rd = a.rd ? a.rd[x] : 1.0, pd = a.pd ? a.pd[x] : 0.0;
-      const int code = check_user(a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], rd, a.pu[x], pd,
-                                  a.arr[x], a.dl[x]);
-      if (code != COINFER_ST_OK) atomicMin(&misc[MI_STATUS], m * 32 + code);
-      fsc[m] = a.dl[x];
-    }
-    const bool simple = __syncthreads_and(M == 0 || [&] {
-      bool z = true;
-      for (int m = tid; m < M; m += NT) z = z && a.arr[base + m] == 0.0 && a.fmin[base + m] == 0.0;
-      return z;
-    }());
-    int status = misc[MI_STATUS];
-    if (P.bmax < M) status = COINFER_ST_SHORT_TABLE;  // checked before the users
-    else if (status != INT_MAX) status &= 31;
-    else status = COINFER_ST_OK;
-    if (status != COINFER_ST_OK) {
-      if (tid == 0) {
-        if (a.do_ip && a.ip.status) a.ip.status[k] = status;
-        if (a.do_og && a.og.status) a.og.status[k] = status;
-      }
-      __syncthreads();
-      continue;
-    }
-    // stable rank by (deadline, id): std::sort with std::tie (offline_solvers.hpp:292-296)
-    for (int m = tid; m < M; m += NT) {
-      const double d = fsc[m];
-      int r = 0;
-      for (int o = 0; o < M; ++o) {
-        const double e = fsc[o];
-        r += (e < d) || (e == d && o < m);
-      }
-      rank[m] = r;
-      order[r] = m;
-      dls[r] = d;
-      const size_t x = base + m;
-      build_rec<N>(rec + r * REC, P, a.fmin[x], a.fmax[x], a.kappa[x], a.ru[x], a.pu[x], a.arr[x], d);
-    }
-    __syncthreads();
-
-    // ---------------------------------------- phase 1: chains per row, init
-    const int nip = a.do_ip ? 1 : 0;
-    const int Q = nip + (a.do_og ? M : 0);
-    // IP-SSA common deadline: caller's, else min_m l_m (coinfer_main.cpp:240-243)
-    const double l_ip = (a.do_ip && a.l_ip) ? a.l_ip[k] : dls[0];
-    for (int q = tid; q < Q; q += NT) {
-      const bool isip = q < nip;
-      const int row = q - nip;
-      const int len = isip ? M : M - row;
-      const double d = isip ? l_ip : dls[row];
-      const int b0 = first_infeasible<N>(a.lat, P.bmax, d, len);
-      b0s[q] = b0;
-      const int cnt = b0 < len ? b0 : len;  // chains of this row
-      rowoff[q + 1] = (cnt + K - 1) / K;     // lane tuples of K chains, prefix-summed below
-    }
-    for (int sz = tid + 1; sz <= M; sz += NT) {  // sum_latency (offline_solvers.hpp:42-47)
-      double t = 0.0;
-      for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __ldg(a.lat + (size_t)(n - 1) * P.bmax + sz - 1));
-      sumlat[sz] = t;
-    }
-    if (a.do_og)
-      for (int x = tid; x < M * (M + 1) / 2; x += NT) tri[x] = INF;
-    __syncthreads();
-    if (tid == 0) {
-      rowoff[0] = 0;
-      for (int q = 0; q < Q; ++q) rowoff[q + 1] += rowoff[q];
-      miscd[0] = INF;  // IP-SSA best energy
-      ipb[0] = 0;
-    }
-    __syncthreads();
-
-    CFB_MARK(0);
-    // ------------------------------------------------- phase 2: G table rows
-    // Warp tasks = 32 consecutive chains of the flat list.  Each warp owns a
-    // contiguous range of tasks balanced by step count, so a row split
-    // between two tasks of the same warp is merged in place (in b order);
-    // only the row a warp inherits from the previous warp's range goes to
-    // that warp's head buffer, merged after the single barrier below.
-    const int C = rowoff[Q];
-    const int ntask = (C + 31) >> 5;
-    for (int t = tid; t < ntask; t += NT) {
-      const int c = t * 32;
-      int lo = 0, hi = Q - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (rowoff[mid] <= c) lo = mid; else hi = mid - 1;
-      }
-      tpre[t + 1] = (lo < nip ? M : M - (lo - nip)) + 4;  // steps + setup
-    }
-    __syncthreads();
-    if (tid == 0) {
-      tpre[0] = 0;
-      for (int t = 0; t < ntask; ++t) tpre[t + 1] += tpre[t];
-    }
-    __syncthreads();
-    {
-      // this warp's task range [t0, t1): balanced prefix cut
-      const int total_cost = tpre[ntask];
-      auto cut = [&](int w) {
-        const int target = (int)(((long long)total_cost * w) / W);
-        int lo = 0, hi = ntask;  // first t with tpre[t] >= target
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (tpre[mid] < target) lo = mid + 1; else hi = mid;
-        }
-        return lo;
-      };
-      const int t0 = cut(warp), t1 = cut(warp + 1);
-      const int c0 = t0 * 32;  // first chain of this warp's range
-      // head buffer: the row (if any) that started in an earlier warp's range
-      int hq = -1, hlen = 0;
-      if (t0 < t1) {
-        int lo = 0, hi = Q - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (rowoff[mid] <= c0) lo = mid; else hi = mid - 1;
-        }
-        if (rowoff[lo] < c0) {
-          hq = lo;
-          hlen = lo < nip ? M : M - (lo - nip);
-        }
-      }
-      for (int kk = lane; kk < hlen; kk += 32) headE[warp * M + kk] = INF;
-      if (lane == 0) {
-        headq[warp] = hq;
-        headlen[warp] = hlen;
-      }
-      __syncwarp();
-      const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
-      const uint32_t RECB = (uint32_t)(REC * 8);
-      bool num_ok = true;  // div.rn.f64 fast-path numerator test, once per launch
-#pragma unroll
-      for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(P.prefix[n]);
-      for (int t = t0; t < t1; ++t) {
-        // ---- per-lane setup: lane = one pair of chains (b, b+1) of one row
-        const int c = t * 32 + lane;
-        const bool has = c < C;
-        const int cc = has ? c : C - 1;
-        int lo = 0, hi = Q - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (rowoff[mid] <= cc) lo = mid; else hi = mid - 1;
-        }
-        const int q = lo;
-        const bool isip = q < nip;
-        const int row = q - nip;
-        const int qlo = rowoff[q];
-        const int b0q = b0s[q];
-        const int len = isip ? M : M - row;
-        const int cnt = b0q < len ? b0q : len;
-        const int b1 = K * (cc - qlo) + 1;  // first bound of this lane's K chains
-        bool al[K], alive[K];
-        int bk[K], kmin[K], off[K];
-        double s[K][N], tot[K];
-        const double dlq = isip ? l_ip : dls[row];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          bk[k] = b1 + k;
-          alive[k] = has && bk[k] <= cnt;
-          al[k] = bk[k] == b0q;
-          // candidate window: group sizes kk+1 >= b (all-local: >= b0), IP only at the end
-          kmin[k] = isip ? M - 1 : (al[k] ? b0q - 1 : bk[k] - 1);
-          off[k] = 0;
-          tot[k] = 0.0;
-          if (alive[k] && !al[k]) {
-            start_times<N>(a.lat, P.bmax, dlq, bk[k], s[k]);
-          } else {
-#pragma unroll
-            for (int n = 0; n < N; ++n) s[k][n] = -1.0;
-          }
-        }
-        const uint32_t rb0 = rec_s + (uint32_t)(isip ? 0 : row) * RECB;
-        uint32_t tE0, tB0;
-        if (qlo < c0) {  // row inherited from the previous warp's range: head buffer
-          tE0 = (uint32_t)__cvta_generic_to_shared(headE + warp * M);
-          tB0 = (uint32_t)__cvta_generic_to_shared(headb + warp * M);
-        } else if (isip) {
-          tE0 = (uint32_t)__cvta_generic_to_shared(miscd) - 8u * (uint32_t)(M - 1);
-          tB0 = (uint32_t)__cvta_generic_to_shared(ipb) - (uint32_t)(M - 1);
-        } else {
-          const int x = tri_idx(row, row, M);
-          tE0 = (uint32_t)__cvta_generic_to_shared(tri + x);
-          tB0 = (uint32_t)__cvta_generic_to_shared(bstar + x);
-        }
-        const int steps = __shfl_sync(kFull, len, 0);
-        const int nvalid = min(32, C - t * 32);
-        const int seg_lo = has ? max(qlo - t * 32, 0) : nvalid;
-        const int seg_hi = has ? min(rowoff[q + 1] - t * 32, nvalid) : 32;
-        const unsigned segmask =
-            (seg_hi >= 32 ? kFull : ((1u << seg_hi) - 1u)) & ~((1u << seg_lo) - 1u);
-        auto steploop = [&](auto tag) {
-        for (int kk = 0; kk < steps; ++kk) {
-          bool live[K], any_live = false;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            live[k] = alive[k] && kk < len;
-            any_live = any_live || live[k];
-          }
-          if (any_live) {
-            const uint32_t rb = isip ? rec_s + (uint32_t)rank[kk] * RECB : rb0 + (uint32_t)kk * RECB;
-            int sp[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) sp[k] = 0;
-            eval_multi<N, K, decltype(tag)::value>(rb, P, s, al, num_ok, live, tot, sp);
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-              if (live[k]) {
-                alive[k] = sp[k] >= 0;
-                off[k] += (sp[k] >= 0 && sp[k] < N);
-              }
-          }
-          // in-lane argmin first: a later chain (larger b) wins ties
-          bool cand = false;
-          double tbest = 0.0;
-          unsigned short wb = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const bool ck = alive[k] && kk >= kmin[k] && kk < len && off[k] <= bk[k];
-            if (ck && (!cand || tot[k] <= tbest)) {
-              tbest = tot[k];
-              wb = (unsigned short)(al[k] ? kk + 1 : bk[k]);  // all-local: largest admissible b
-            }
-            cand = cand || ck;
-          }
-          {
-            // segmented lexicographic argmin over the lanes of each row
-            // segment with redux.sync on the 64-bit energy bits (energies are
-            // >= +0, so the unsigned bit order is the numeric order); lanes
-            // of a segment hold ascending b, so the highest tied lane wins
-            const unsigned long long key = (unsigned long long)__double_as_longlong(tbest);
-            const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
-            const unsigned mh = __reduce_min_sync(segmask, cand ? khi : 0xffffffffu);
-            const bool hit = cand && khi == mh;
-            unsigned wm = __ballot_sync(kFull, hit) & segmask;
-            if (__any_sync(kFull, __popc(wm) > 1)) {  // a tie in the high word: low word decides
-              const unsigned ml = __reduce_min_sync(segmask, hit ? klo : 0xffffffffu);
-              wm = __ballot_sync(kFull, hit && klo == ml) & segmask;
-            }
-            if (wm != 0u && lane == 31 - __clz(wm)) {
-              const uint32_t aE = tE0 + 8u * (uint32_t)kk, aB = tB0 + (uint32_t)kk;
-              double cur;
-              asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cur) : "r"(aE) : "memory");
-              if (tbest <= cur) {  // later chains carry larger b: they win ties
-                asm volatile("st.shared.f64 [%0], %1;" ::"r"(aE), "d"(tbest) : "memory");
-                asm volatile("st.shared.u8 [%0], %1;" ::"r"(aB), "h"(wb) : "memory");
-              }
-            }
-          }
-        }
-        };
-        if (simple)
-          steploop(std::true_type{});
-        else
-          steploop(std::false_type{});
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      for (int w = 1; w < W; ++w) {
-        const int hl = headlen[w];
-        if (hl == 0) continue;
-        const int q = headq[w];
-        const bool isip = q < nip;
-        const int row = q - nip;
-        for (int kk = lane; kk < hl; kk += 32) {
-          const double e = headE[w * M + kk];
-          if (e == INF) continue;
-          const int hb = headb[w * M + kk];
-          if (isip) {
-            if (kk == M - 1 && e <= miscd[0]) {
-              miscd[0] = e;
-              ipb[0] = (uint8_t)hb;
-            }
-          } else {
-            const int x = tri_idx(row, row + kk, M);
-            if (e <= tri[x]) {
-              tri[x] = e;
-              bstar[x] = (uint8_t)hb;
-            }
-          }
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-
-    CFB_MARK(1);
-    // ------------------------------------------------- phase 3: IP-SSA output
-    if (a.do_ip) {
-      const double ipE = miscd[0];
-      const int ipbv = ipb[0];
-      if (ipE == INF) {
-        if (tid == 0 && a.ip.status) a.ip.status[k] = COINFER_ST_INFEASIBLE;
-      } else {
-        const bool pipe = ipbv < b0s[0];
-        double s[N];
-        if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipbv, s);
-        else
-#pragma unroll
-          for (int n = 0; n < N; ++n) s[n] = 0.0;
-        for (int m = tid; m < M; m += NT) {
-          const double* r = rec + rank[m] * REC;
-          int sp;
-          double f;
-          choose<N>(r, P, s, pipe, sp, f);
-          const size_t x = base + m;
-          if (a.ip.split) a.ip.split[x] = (uint8_t)sp;
-          if (a.ip.freq) a.ip.freq[x] = f;
-          if (a.ip.user_energy) a.ip.user_energy[x] = fold<N>(r, sp, f, 0.0);
-          spsc[rank[m]] = (uint8_t)sp;
-        }
-        if (tid == 0) {
-          if (a.ip.status) a.ip.status[k] = COINFER_ST_OK;
-          if (a.ip.batch_bound) a.ip.batch_bound[k] = ipbv;
-          if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[k] = pipe;
-          if (a.ip.energy) a.ip.energy[k] = ipE;
-        }
-        __syncthreads();
-        if (a.ip.batch_size)
-          for (int n = 1 + tid; n <= N; n += NT) {
-            int c = 0;
-            for (int x = 0; x < M; ++x) c += spsc[x] < n;
-            a.ip.batch_size[(size_t)k * N + n - 1] = c;
-          }
-      }
-      __syncthreads();
-    }
-    if (!a.do_og) continue;
-
-    CFB_MARK(2);
-    // ---------------------------------------------------- phase 4: OG DP
-    // S[i][j] = min over feasible prev < i of S[prev][i-1] + G[i][j], strict
-    // '<' so the smallest prev wins ties (offline_solvers.hpp:313-330); in
-    // place over the triangle (S[0][j] = G[0][j] already).  Stage i: Qp
-    // threads per cell j split the prevs (strided), each keeps a running
-    // lexicographic (value, prev) minimum, and the Qp partials combine by the
-    // same order, which equals the reference's ascending scan.  groups_fit is
-    // monotone in prev (sorted deadlines), so a thread stops at its first
-    // infeasible prev.
-    for (int i = 1; i < M; ++i) {
-      const int nj = M - i;
-      int Qp = 1;  // threads per cell, a power of two <= 32
-      while (Qp < 32 && nj * Qp * 2 <= NT && Qp < i) Qp <<= 1;
-      const int pairs = nj * Qp;
-      const double di = dls[i];
-      const int col = tri_idx(0, i - 1, M);  // S[0][i-1]; S[p][i-1] = col + p*(M-1) - p(p-1)/2
-      for (int t0 = 0; t0 < pairs; t0 += NT) {
-        const int t = t0 + tid;
-        const bool act = t < pairs;
-        const int j = i + (act ? t / Qp : 0);
-        const int qq = t & (Qp - 1);
-        double best = INF;
-        int bp = 255;
-        if (act) {
-          const double g = tri[tri_idx(i, j, M)];
-          if (g != INF) {
-            const double thr = sumlat[j - i + 1];
-            for (int prev = qq; prev < i; prev += Qp) {
-              if (!(__dadd_rn(dls[prev], thr) <= di)) break;  // groups_fit, prefix in prev
-              const double sp = tri[col + prev * (M - 1) - ((prev * (prev - 1)) >> 1)];
-              const double cand = __dadd_rn(sp, g);
-              if (sp != INF && cand < best) {
-                best = cand;
-                bp = prev;
-              }
-            }
-          }
-        }
-        for (int off = 1; off < Qp; off <<= 1) {
-          const double ob = __shfl_xor_sync(kFull, best, off);
-          const int op = __shfl_xor_sync(kFull, bp, off);
-          if (ob < best || (ob == best && op < bp)) {
-            best = ob;
-            bp = op;
-          }
-        }
-        if (act && qq == 0) {
-          const int x = tri_idx(i, j, M);
-          tri[x] = best;
-          parent[x] = (uint8_t)bp;
-        }
-      }
-      __syncthreads();
-    }
-
-    CFB_MARK(3);
-    // best_i: strict '<', smallest i (offline_solvers.hpp:332-334)
-    if (warp == 0) {
-      double bv = INF;
-      int bi = M;
-      for (int i = lane; i < M; i += 32) {
-        const double v = tri[tri_idx(i, M - 1, M)];
-        if (v < bv || (v == bv && i < bi)) {
-          bv = v;
-          bi = i;
-        }
-      }
-      for (int off = 16; off; off >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, bv, off);
-        const int oi = __shfl_xor_sync(kFull, bi, off);
-        if (ov < bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if (lane == 0) {
-        misc[MI_BESTI] = (bv == INF) ? -1 : bi;
-        miscd[1] = bv;
-        misc[MI_OGST] = COINFER_ST_OK;
-      }
-    }
-    __syncthreads();
-    const int best_i = misc[MI_BESTI];
-    if (a.og.order)
-      for (int i = tid; i < M; i += NT) a.og.order[base + i] = order[i];
-
-    if (best_i < 0) {
-      // ------------------------------ lc_solve fallback (offline_solvers.hpp:336-348)
-      for (int i = tid; i < M; i += NT) {
-        const double* r = rec + i * REC;
-        if (r[R::FEAS] == 0.0) misc[MI_OGST] = COINFER_ST_INFEASIBLE;
-      }
-      __syncthreads();
-      if (misc[MI_OGST] != COINFER_ST_OK) {
-        if (tid == 0 && a.og.status) a.og.status[k] = COINFER_ST_INFEASIBLE;
-        __syncthreads();
-        continue;
-      }
-      for (int i = tid; i < M; i += NT) {
-        const double* r = rec + i * REC;
-        const double fL = r[R::FL];
-        const double e = fold<N>(r, N, fL, 0.0);
-        const int m = order[i];
-        const size_t g = base + i;
-        if (a.og.group_lo) a.og.group_lo[g] = i;
-        if (a.og.group_size) a.og.group_size[g] = 1;
-        if (a.og.group_b) a.og.group_b[g] = 0;
-        if (a.og.group_deadline) a.og.group_deadline[g] = dls[i];
-        if (a.og.group_energy) a.og.group_energy[g] = e;
-        if (a.og.group_batch_size)
-          for (int n = 0; n < N; ++n) a.og.group_batch_size[g * N + n] = 0;
-        if (a.og.group_of_user) a.og.group_of_user[base + m] = i;
-        if (a.og.split) a.og.split[base + m] = (uint8_t)N;
-        if (a.og.freq) a.og.freq[base + m] = fL;
-        if (a.og.user_energy) a.og.user_energy[base + m] = e;
-      }
-      if (tid == 0) {
-        double total = 0.0;  // lc_solve folds users in original order
-        for (int m = 0; m < M; ++m) {
-          const double* r = rec + rank[m] * REC;
-          total = fold<N>(r, N, r[R::FL], total);
-        }
-        if (a.og.status) a.og.status[k] = COINFER_ST_OK;
-        if (a.og.fallback) a.og.fallback[k] = 1;
-        if (a.og.energy) a.og.energy[k] = total;
-        if (a.og.n_groups) a.og.n_groups[k] = M;
-      }
-      __syncthreads();
-      continue;
-    }
-
-    // ------------------------------- backtrack (offline_solvers.hpp:350-360)
-    if (tid == 0) {
-      int ng = 0, i = best_i, j = M - 1;
-      while (true) {
-        glo[ng] = i;
-        ghi[ng] = j;
-        ++ng;
-        if (i == 0) break;
-        const int prev = parent[tri_idx(i, j, M)];
-        j = i - 1;
-        i = prev;
-      }
-      for (int x = 0, y = ng - 1; x < y; ++x, --y) {
-        int tt = glo[x];
-        glo[x] = glo[y];
-        glo[y] = tt;
-        tt = ghi[x];
-        ghi[x] = ghi[y];
-        ghi[y] = tt;
-      }
-      misc[MI_NG] = ng;
-    }
-    __syncthreads();
-    const int ng = misc[MI_NG];
-    for (int g = tid; g < ng; g += NT)
-      for (int x = glo[g]; x <= ghi[g]; ++x) gid[x] = g;
-    __syncthreads();
-
-    // --------------------------- stitch: re-derive every chosen group's plan
-    for (int j = tid; j < M; j += NT) {
-      const int g = gid[j];
-      const int lo = glo[g], hi = ghi[g];
-      const int bb = bstar[tri_idx(lo, hi, M)];
-      const bool pipe = bb < b0s[nip + lo];
-      double s[N];
-      if (pipe) start_times<N>(a.lat, P.bmax, dls[lo], bb, s);
-      else
-#pragma unroll
-        for (int n = 0; n < N; ++n) s[n] = 0.0;
-      const double* r = rec + j * REC;
-      int sp;
-      double f;
-      choose<N>(r, P, s, pipe, sp, f);
-      spsc[j] = (uint8_t)sp;
-      fsc[j] = f;
-      const int m = order[j];
-      if (a.og.group_of_user) a.og.group_of_user[base + m] = g;
-      if (a.og.split) a.og.split[base + m] = (uint8_t)sp;
-      if (a.og.freq) a.og.freq[base + m] = f;
-      if (a.og.user_energy) a.og.user_energy[base + m] = fold<N>(r, sp, f, 0.0);
-    }
-    __syncthreads();
-    for (int g = tid; g < ng; g += NT) {
-      const int lo = glo[g], hi = ghi[g];
-      double total = 0.0;
-      for (int x = lo; x <= hi; ++x) total = fold<N>(rec + x * REC, spsc[x], fsc[x], total);
-      sumlat[g] = total;  // group energies (sumlat no longer needed)
-      const size_t gi = base + g;
-      if (a.og.group_lo) a.og.group_lo[gi] = lo;
-      if (a.og.group_size) a.og.group_size[gi] = hi - lo + 1;
-      if (a.og.group_b) a.og.group_b[gi] = bstar[tri_idx(lo, hi, M)];
-      if (a.og.group_deadline) a.og.group_deadline[gi] = dls[lo];
-      if (a.og.group_energy) a.og.group_energy[gi] = total;
-      if (a.og.group_batch_size)
-        for (int n = 1; n <= N; ++n) {
-          int c = 0;
-          for (int x = lo; x <= hi; ++x) c += spsc[x] < n;
-          a.og.group_batch_size[gi * N + n - 1] = c;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double e = 0.0;  // plan.energy: left fold of group energies (:385-386)
-      for (int g = 0; g < ng; ++g) e = __dadd_rn(e, sumlat[g]);
-      if (a.og.status) a.og.status[k] = COINFER_ST_OK;
-      if (a.og.fallback) a.og.fallback[k] = 0;
-      if (a.og.energy) a.og.energy[k] = e;
-      if (a.og.n_groups) a.og.n_groups[k] = ng;
-    }
-    CFB_MARK(4);
+    InstIn in;
+    in.fmin = a.fmin + base;
+    in.fmax = a.fmax + base;
+    in.kappa = a.kappa + base;
+    in.ru = a.ru + base;
+    in.pu = a.pu + base;
+    in.arr = a.arr + base;
+    in.dl = a.dl + base;
+    in.rd = a.rd ? a.rd + base : nullptr;
+    in.pd = a.pd ? a.pd + base : nullptr;
+    in.has_l_ip = a.l_ip != nullptr;
+    in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
+    solve_one<N>(a, k, base, M, in, sm, a.L);
   }
 }
 
@@ -846,26 +184,6 @@ static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid
   return cudaGetLastError();
 }
 
-#define CFB_DISPATCH_N(NVAL, CALL) \
-  switch (NVAL) {                  \
-    case 1: CALL(1); break;        \
-    case 2: CALL(2); break;        \
-    case 3: CALL(3); break;        \
-    case 4: CALL(4); break;        \
-    case 5: CALL(5); break;        \
-    case 6: CALL(6); break;        \
-    case 7: CALL(7); break;        \
-    case 8: CALL(8); break;        \
-    case 9: CALL(9); break;        \
-    case 10: CALL(10); break;      \
-    case 11: CALL(11); break;      \
-    case 12: CALL(12); break;      \
-    case 13: CALL(13); break;      \
-    case 14: CALL(14); break;      \
-    case 15: CALL(15); break;      \
-    case 16: CALL(16); break;      \
-    default: return cudaErrorInvalidValue; \
-  }
 
 #ifdef CFB_PHASE_TIMING
 extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {

@@ -259,3 +259,71 @@ class Engine:
             self.ctx, C.byref(pk.profile), C.byref(pk.users),
             C.byref(pk.out_ip) if ipssa else None, C.byref(pk.out_og) if og else None))
         return Packed.arrays(pk.out_ip), Packed.arrays(pk.out_og)
+
+
+@dataclass
+class OnlineConfig:
+    """ArrivalModel + OnlineEnv + policy settings (online_sim.hpp:26-39,69-91,301-336)."""
+    arrival: str = "bernoulli"   # or "immediate"
+    p_arrive: float = 0.25
+    l_low: float = 0.25
+    l_high: float = 1.0
+    slot: float = 0.025
+    solver: str = "og"           # or "ipssa"
+    policy: str = "tw"           # TimeWindowPolicy(window, l_high), or "local"
+    window: int = 0
+    threshold: Optional[float] = None  # TimeWindowPolicy threshold; None = l_high (the CLI's choice)
+    horizon: int = 100_000
+
+    def to_c(self) -> "_abi.OnlineCfg":
+        return _abi.OnlineCfg(
+            _abi.ARRIVAL_IMMEDIATE if self.arrival == "immediate" else _abi.ARRIVAL_BERNOULLI,
+            _abi.SOLVER_OG if self.solver == "og" else _abi.SOLVER_IPSSA,
+            _abi.POLICY_LOCAL if self.policy == "local" else _abi.POLICY_TW,
+            int(self.window), float(self.p_arrive), float(self.l_low), float(self.l_high),
+            float(self.slot), float(self.l_high if self.threshold is None else self.threshold),
+            int(self.horizon))
+
+
+def _online(self, profile, scenarios: Dict, cfg: OnlineConfig, seeds, n_trace: int = 0):
+    """run_episode for every seed (one GPU warp per episode).  Episode e runs
+    scenario e % n_scenarios.  Returns status, totals [E,3] (total_energy,
+    total_forced_cost, total_reward), counts [E,6] (forced_count,
+    solver_calls, solver_tasks, solver_groups, batches, batched_tasks) and,
+    for the first n_trace episodes, per-slot reward/energy/pending/edge_busy."""
+    mem = self._mem(scenarios)
+    pk = Packed(profile, scenarios, mem, False, False)
+    E = int(len(seeds))
+    T = int(n_trace) * int(cfg.horizon)
+    dev = f"cuda:{self.device}"
+
+    def alloc(shape, np_dtype, t_dtype):
+        if mem == _abi.MEM_DEVICE:
+            return torch.zeros(shape, dtype=t_dtype, device=dev)
+        return np.zeros(shape, dtype=np_dtype)
+
+    if mem == _abi.MEM_DEVICE:
+        sd = seeds if _is_torch(seeds) else torch.as_tensor(np.asarray(seeds, dtype=np.uint64).view(np.int64), device=dev)
+    else:
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    out = dict(status=alloc((E,), np.int32, torch.int32 if torch else None),
+               totals=alloc((E, 3), np.float64, torch.float64 if torch else None),
+               counts=alloc((E, 6), np.int64, torch.int64 if torch else None))
+    if T:
+        out.update(trace_reward=alloc((n_trace, cfg.horizon), np.float64, torch.float64),
+                   trace_energy=alloc((n_trace, cfg.horizon), np.float64, torch.float64),
+                   trace_pending=alloc((n_trace, cfg.horizon), np.int32, torch.int32),
+                   trace_edge_busy=alloc((n_trace, cfg.horizon), np.float64, torch.float64))
+    oo = _abi.OnlineOut(_ptr(out["status"], C.c_int32), _ptr(out["totals"], C.c_double),
+                        _ptr(out["counts"], C.c_int64), int(n_trace) if T else 0,
+                        _ptr(out.get("trace_reward"), C.c_double),
+                        _ptr(out.get("trace_energy"), C.c_double),
+                        _ptr(out.get("trace_pending"), C.c_int32),
+                        _ptr(out.get("trace_edge_busy"), C.c_double))
+    c = cfg.to_c()
+    self._check(self.lib.coinfer_online_run(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                            C.byref(c), _ptr(sd, C.c_uint64), E, C.byref(oo)))
+    return out
+
+
+Engine.online = _online

@@ -54,7 +54,7 @@ REF_SYMBOLS = {
     "ref_sample_scenario": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                       C.c_uint64] + [_dp] * 9),
     "ref_online_episode": (C.c_int, [_P, _U, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
-                                     C.c_double, C.c_uint64, C.c_int, C.c_int64, _dp,
+                                     C.c_double, C.c_uint64, C.c_int, C.c_double, C.c_int64, _dp,
                                      C.POINTER(C.c_int64), _dp, _dp, _i32p, _dp]),
 }
 
@@ -249,3 +249,25 @@ def ref_sample_scenarios(n_inst, M, low, high, seeds, heavy=True, bandwidth=1e6)
 
 def slice_users(u, k0, k1):
     return {n: v[k0:k1] for n, v in u.items()}
+
+
+def ref_online(profile, users, cfg, seed, trace=True):
+    """run_episode(OnlineEnv(scenario 0 of users, ...), TimeWindowPolicy(window, l_high),
+    horizon, seed) through the reference (needs oracle/_ref).  Returns a dict
+    like Engine.online for one episode."""
+    import ctypes as C
+    pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+    H = int(cfg.horizon)
+    totals = np.zeros(4)
+    counts = np.zeros(6, dtype=np.int64)
+    rw, en, bu = np.zeros(H), np.zeros(H), np.zeros(H)
+    pe = np.zeros(H, dtype=np.int32)
+    rc = ref().ref_online_episode(
+        C.byref(pk.profile), C.byref(pk.users), 1 if cfg.solver == "og" else 0, cfg.p_arrive,
+        1 if cfg.arrival == "immediate" else 0, cfg.l_low, cfg.l_high, cfg.slot, int(seed),
+        -1 if cfg.policy == "local" else int(cfg.window),
+        cfg.l_high if cfg.threshold is None else cfg.threshold, H, totals.ctypes.data_as(_dp), counts.ctypes.data_as(C.POINTER(C.c_int64)),
+        rw.ctypes.data_as(_dp), en.ctypes.data_as(_dp), pe.ctypes.data_as(_i32p),
+        bu.ctypes.data_as(_dp))
+    return dict(rc=rc, totals=totals[:3], counts=counts, trace_reward=rw, trace_energy=en,
+                trace_pending=pe, trace_edge_busy=bu)

@@ -231,8 +231,51 @@ def cli_cases():
     return out
 
 
+def online_cases():
+    """run_episode traces from the reference: the reference tests' own online
+    setups (test_online_sim.cpp) and CLI-style episodes (coinfer_main.cpp:482-573)."""
+    from paper_2206_06304_b200.engine import OnlineConfig
+    out = []
+
+    def ep(name, prof, u, cfg, seed):
+        r = ck.ref_online(prof, u, cfg, seed)
+        assert r["rc"] == 0, name
+        out.append(dict(name=name, profile=dict(work=enc(prof.work), data_bits=enc(prof.data_bits),
+                                                latency=enc(prof.latency)),
+                        users={k: enc(v) for k, v in u.items()}, cfg=cfg.__dict__, seed=int(seed),
+                        expect={k: enc(v) for k, v in r.items() if k != "rc"}))
+
+    # test_online_sim.cpp:231-248, 250-268, 320-335, 157-176, 209-229
+    p, u = ck.two_stage(3)
+    ep("accounting_og_tw1", p, u, OnlineConfig("bernoulli", 0.35, 0.1, 0.4, 0.025, "og", "tw", 1, 0.4, 400), 23)
+    p, u = ck.two_stage(4)
+    ep("reproduce_ipssa_tw2", p, u, OnlineConfig("bernoulli", 0.4, 0.1, 0.4, 0.025, "ipssa", "tw", 2, 0.4, 250), 31)
+    p, u = ck.two_stage(5)
+    ep("deadline_safe_og_tw3", p, u, OnlineConfig("bernoulli", 0.6, 0.08, 0.5, 0.025, "og", "tw", 3, 0.2, 600), 41)
+    ep("deadline_safe_ipssa_tw3", p, u, OnlineConfig("bernoulli", 0.6, 0.08, 0.5, 0.025, "ipssa", "tw", 3, 0.2, 600), 41)
+    p, u = ck.two_stage(3)
+    ep("certain_arrival_local", p, u, OnlineConfig("bernoulli", 1.0, 0.1, 0.4, 0.025, "og", "local", 0, None, 200), 17)
+    ep("immediate_local", p, u, OnlineConfig("immediate", 1.0, 0.1, 0.4, 0.025, "og", "local", 0, None, 200), 17)
+    # CLI online path: sample_scenario(users, fixed(l_high)) with sub_seed(root, 1, 0)
+    s0 = R.ref_sub_seed(1, 1, 0)
+    p, u = ck.ref_sample_scenarios(1, 14, 1.0, 1.0, [s0], heavy=True)
+    for ep_i in range(2):
+        ep(f"cli_heavy_og_tw0_ep{ep_i}", p, u, OnlineConfig("bernoulli", 0.05, 0.25, 1.0, 0.025, "og", "tw", 0, None, 4000),
+           R.ref_sub_seed(1, 5, ep_i))
+    ep("cli_heavy_ipssa_tw2", p, u, OnlineConfig("bernoulli", 0.1, 0.25, 1.0, 0.025, "ipssa", "tw", 2, None, 4000),
+       R.ref_sub_seed(1, 5, 7))
+    p, u = ck.ref_sample_scenarios(1, 14, 0.2, 0.2, [s0], heavy=False)
+    ep("cli_light_og_tw0", p, u, OnlineConfig("bernoulli", 0.25, 0.05, 0.2, 0.025, "og", "tw", 0, None, 4000),
+       R.ref_sub_seed(1, 5, 0))
+    p, u = ck.ref_sample_scenarios(1, 6, 1.0, 1.0, [s0], heavy=False)
+    ep("cli_default_light_tw2", p, u, OnlineConfig("bernoulli", 0.25, 0.25, 1.0, 0.025, "og", "tw", 2, None, 2000),
+       R.ref_sub_seed(1, 5, 3))
+    return out
+
+
 def main():
-    for name, fn in [("kat", kat_cases), ("random", random_cases), ("cli", cli_cases)]:
+    for name, fn in [("kat", kat_cases), ("random", random_cases), ("cli", cli_cases),
+                     ("online", online_cases)]:
         cases = fn()
         path = os.path.join(HERE, f"{name}.json")
         with open(path, "w") as f:
