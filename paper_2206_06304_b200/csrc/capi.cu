@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,6 +34,9 @@ struct coinfer_ctx {
   cudaStream_t pipe[2] = {nullptr, nullptr};
   unsigned char* ws2[2] = {nullptr, nullptr};
   size_t ws2_cap[2] = {0, 0};
+  // large-instance path workspace (G/S triangles etc.)
+  unsigned char* big = nullptr;
+  size_t big_cap = 0;
 };
 
 namespace {
@@ -232,6 +236,82 @@ void patch_og_out(unsigned char* b, coinfer_og_out& o) {
 
 constexpr int kSmallMaxM = 255;  // u8 group/bound indices in shared memory
 
+// Instances too large for one CTA's shared memory: the multi-kernel path of
+// solve_large.cu, one instance at a time.  `a` carries device pointers.
+int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st) {
+  const int M = a.M, N = a.P.N;
+  const size_t need = cfb::large_ws_bytes(M, N);
+  if (need > ctx->big_cap) {
+    cudaStreamSynchronize(st);
+    if (ctx->big) cudaFree(ctx->big);
+    ctx->big = nullptr;
+    ctx->big_cap = 0;
+    cudaError_t e = cudaMalloc(&ctx->big, need);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(large workspace)");
+    ctx->big_cap = need;
+  }
+  const size_t T = (size_t)M * (M + 1) / 2;
+  unsigned char* w = ctx->big;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = w;
+    w += (bytes + 255) & ~size_t(255);
+    return p;
+  };
+  cfb::LargeArgs L;
+  std::memset(&L, 0, sizeof L);
+  L.P = a.P;
+  L.lat = a.lat;
+  L.M = M;
+  L.do_ip = a.do_ip;
+  L.do_og = a.do_og;
+  L.G = reinterpret_cast<double*>(take(8 * T));
+  L.St = reinterpret_cast<double*>(take(8 * T));
+  L.bstar = reinterpret_cast<uint16_t*>(take(2 * T));
+  L.par = reinterpret_cast<uint16_t*>(take(2 * T));
+  L.rec = reinterpret_cast<double*>(take((size_t)M * cfb::rec_size(N) * 8));
+  L.dls = reinterpret_cast<double*>(take(8 * (size_t)M));
+  L.sumlat = reinterpret_cast<double*>(take(8 * ((size_t)M + 2)));
+  L.fpos = reinterpret_cast<double*>(take(8 * (size_t)M));
+  L.genergy = reinterpret_cast<double*>(take(8 * (size_t)M));
+  L.ipres = reinterpret_cast<double*>(take(8));
+  L.order = reinterpret_cast<int*>(take(4 * (size_t)M));
+  L.rank = reinterpret_cast<int*>(take(4 * (size_t)M));
+  L.b0 = reinterpret_cast<int*>(take(4 * ((size_t)M + 2)));
+  L.spos = reinterpret_cast<int*>(take(4 * (size_t)M));
+  L.gid = reinterpret_cast<int*>(take(4 * (size_t)M));
+  L.status = reinterpret_cast<int*>(take(4));
+  L.simple = reinterpret_cast<int*>(take(4));
+  L.ipb = reinterpret_cast<uint16_t*>(take(4));
+  L.ip = a.ip;
+  L.og = a.og;
+  for (int64_t k = 0; k < a.n_inst; ++k) {
+    const size_t base = (size_t)k * M;
+    L.k = k;
+    L.base = base;
+    L.fmin = a.fmin + base;
+    L.fmax = a.fmax + base;
+    L.kappa = a.kappa + base;
+    L.ru = a.ru + base;
+    L.pu = a.pu + base;
+    L.arr = a.arr + base;
+    L.dl = a.dl + base;
+    L.rd = a.rd ? a.rd + base : nullptr;
+    L.pd = a.pd ? a.pd + base : nullptr;
+    if (a.l_ip) {  // a device pointer: read it inside the kernels would need a copy
+      double v;
+      cudaError_t e = cudaMemcpyAsync(&v, a.l_ip + k, 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "read IP-SSA deadline");
+      L.l_ip = v;
+      L.has_l_ip = 1;
+    }
+    cudaError_t e = cfb::launch_large(L, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "large-instance launch");
+    ctx->launches += 5;
+  }
+  return COINFER_OK;
+}
+
 enum class Mode { Solve, Fixed };
 
 int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* users,
@@ -252,8 +332,6 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   if (mode == Mode::Fixed && users->n_inst > 0 && !bvec)
     return fail(ctx, COINFER_E_ARG, "fixed: null batch-bound array");
   if (users->n_inst == 0) return COINFER_OK;
-  if (users->M > kSmallMaxM)
-    return fail(ctx, COINFER_E_UNSUPPORTED, "M above the shared-memory solver's limit");
 
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
@@ -291,8 +369,58 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
     const int threads = Kc >= 1024 ? 128 : 256;
     return cfb::launch_small(args, threads, grid, st);
   };
-  if (mode != Mode::Fixed && cfb::small_smem_bytes((int)M, (int)N, 8) > 227 * 1024)
-    return fail(ctx, COINFER_E_UNSUPPORTED, "instance does not fit in shared memory");
+  static const bool force_large = std::getenv("COINFER_FORCE_LARGE") != nullptr;  // testing aid
+  const bool large = M > (size_t)kSmallMaxM || cfb::small_smem_bytes((int)M, (int)N, 8) > 227 * 1024 ||
+                     (force_large && mode != Mode::Fixed && M > 0);
+  if (large && mode == Mode::Fixed &&
+      (size_t)cfb::fixed_smem_bytes((int)M, (int)N) > 227 * 1024)
+    return fail(ctx, COINFER_E_UNSUPPORTED, "fixed_batch: instance does not fit in shared memory");
+  if (large && mode != Mode::Fixed) {
+    // one instance at a time through solve_large.cu; host batches are staged whole
+    if (users->mem == COINFER_MEM_DEVICE) return run_large_device(ctx, a, ctx->stream);
+    Stager st{ctx};
+    plan_in(st, a.fmin, K * M);
+    plan_in(st, a.fmax, K * M);
+    plan_in(st, a.kappa, K * M);
+    plan_in(st, a.ru, K * M);
+    plan_in(st, a.pu, K * M);
+    plan_in(st, a.arr, K * M);
+    plan_in(st, a.dl, K * M);
+    plan_in(st, a.rd, K * M);
+    plan_in(st, a.pd, K * M);
+    plan_in(st, a.l_ip, K);
+    if (ip_in) plan_ip_out(st, a.ip, K, M, N);
+    if (og_in) plan_og_out(st, a.og, K, M, N);
+    rc = ensure_ws(ctx, 0, st.used);
+    if (rc != COINFER_OK) return rc;
+    unsigned char* b = ctx->ws2[0];
+    cudaStream_t sp = ctx->pipe[0];
+    patch(b, a.fmin);
+    patch(b, a.fmax);
+    patch(b, a.kappa);
+    patch(b, a.ru);
+    patch(b, a.pu);
+    patch(b, a.arr);
+    patch(b, a.dl);
+    patch(b, a.rd);
+    patch(b, a.pd);
+    patch(b, a.l_ip);
+    if (ip_in) patch_ip_out(b, a.ip);
+    if (og_in) patch_og_out(b, a.og);
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+    }
+    rc = run_large_device(ctx, a, sp);
+    if (rc != COINFER_OK) return rc;
+    for (const auto& x : st.back) {
+      e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+    }
+    e = cudaStreamSynchronize(sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "solve");
+    return COINFER_OK;
+  }
 
   if (users->mem == COINFER_MEM_DEVICE) {
     e = launch(a, bdev, K, ctx->stream);
@@ -427,6 +555,7 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_lat) cudaFree(ctx->d_lat);
+  if (ctx->big) cudaFree(ctx->big);
   for (int i = 0; i < 2; ++i) {
     if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);
     if (ctx->ws2[i]) cudaFree(ctx->ws2[i]);

@@ -60,8 +60,31 @@ struct OnlineArgs {
   int32_t* tr_pending;
 };
 
+// Arguments of the large-instance path (solve_large.cu); one instance per
+// launch sequence, all pointers device memory.
+struct LargeArgs {
+  ProfileConst P;
+  const double* lat;
+  int M;
+  const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl, *rd, *pd;  // this instance
+  double l_ip;
+  int has_l_ip, do_ip, do_og;
+  int64_t k;    // output instance index
+  size_t base;  // output row (k * M)
+  // workspace
+  int* status;  // INT_MAX, or the first failing user * 32 + code
+  int* simple;  // all arrivals and f_min zero
+  double *rec, *dls, *sumlat, *G, *St, *ipres, *fpos, *genergy;
+  int *order, *rank, *b0, *spos, *gid;
+  uint16_t *bstar, *par, *ipb;
+  coinfer_ipssa_out ip;
+  coinfer_og_out og;
+};
+
 int small_smem_bytes(int M, int N, int W);
 int online_smem_bytes(int M, int N);
+size_t large_ws_bytes(int M, int N);
+cudaError_t launch_large(const LargeArgs& a, cudaStream_t st);
 cudaError_t launch_online(const OnlineArgs& a, int grid, cudaStream_t st);
 int fixed_smem_bytes(int M, int N);
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st);

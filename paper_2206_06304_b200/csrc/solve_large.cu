@@ -1,0 +1,492 @@
+// solve_large.cu — IP-SSA / OG for instances too large for shared memory
+// (BASELINE config 4: M = 4096 users in one instance).
+//
+// Same algorithm and bit-exact semantics as solve_core.cuh (see the comments
+// there and in solve_small.cu); only the data placement and the work split
+// differ:
+//   large_prep    one thread per user: contract check, stable deadline rank,
+//                 hoisted records (global, sorted order), sum_latency table
+//   large_rows    one thread per row: first infeasible bound b0 (row 0 is the
+//                 IP-SSA row when requested)
+//   large_grow    one warp per G row (group start i): chains b = 1..cnt in
+//                 passes of 32 lanes, each pass one left fold over j; the
+//                 warp-wide lexicographic argmin (energy asc, b desc) per cell
+//                 merges into the row with `<=` (later passes carry larger b)
+//   large_finish  one CTA: the grouping DP over M sequential stages
+//                 (offline_solvers.hpp:313-330) with the column S[.][i-1] kept
+//                 as a prefix minimum in shared memory, so each cell is two
+//                 binary searches (value, then the reference's smallest prev);
+//                 best_i, backtrack, stitch, lc fallback, IP-SSA outputs.
+// G is an upper triangle in global memory; S is stored transposed (lower
+// triangle, St[j][p] = S[p][j]) so a stage reads its column contiguously.
+
+#include "solve_core.cuh"
+
+namespace cfb {
+
+namespace {
+
+__device__ __forceinline__ long long tri_u(long long i, long long j, long long M) {
+  return i * M - ((i * (i - 1)) >> 1) + (j - i);  // upper triangle, row-major
+}
+__device__ __forceinline__ long long tri_l(long long j, long long p) {
+  return ((j * (j + 1)) >> 1) + p;  // lower triangle: row j holds p = 0..j
+}
+
+}  // namespace
+
+template <int N>
+__global__ void large_prep(LargeArgs a) {
+  using R = Rec<N>;
+  const int M = a.M;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < M) {
+    const double rd = a.rd ? a.rd[m] : 1.0, pd = a.pd ? a.pd[m] : 0.0;
+    const int code = check_user(a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], rd, a.pu[m], pd,
+                                a.arr[m], a.dl[m]);
+    if (code != COINFER_ST_OK && *a.status != COINFER_ST_SHORT_TABLE) atomicMin(a.status, m * 32 + code);
+    if (!(a.arr[m] == 0.0 && a.fmin[m] == 0.0)) atomicAnd(a.simple, 0);
+    const double d = a.dl[m];
+    int r = 0;
+    for (int o = 0; o < M; ++o) {  // stable rank by (deadline, id), offline_solvers.hpp:292-296
+      const double e = __ldg(a.dl + o);
+      r += (e < d) || (e == d && o < m);
+    }
+    a.rank[m] = r;
+    a.order[r] = m;
+    a.dls[r] = d;
+    build_rec<N>(a.rec + (size_t)r * R::SIZE, a.P, a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], a.pu[m],
+                 a.arr[m], d);
+  }
+  if (m >= 1 && m <= M) {  // sum_latency(size = m), offline_solvers.hpp:42-47
+    double t = 0.0;
+    for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __ldg(a.lat + (size_t)(n - 1) * a.P.bmax + m - 1));
+    a.sumlat[m] = t;
+  }
+}
+
+template <int N>
+__global__ void large_rows(LargeArgs a) {
+  if (*a.status != INT_MAX) return;
+  const int M = a.M, nip = a.do_ip ? 1 : 0, Q = nip + (a.do_og ? M : 0);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Q) return;
+  const bool isip = q < nip;
+  const int len = isip ? M : M - (q - nip);
+  const double d = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[q - nip];
+  a.b0[q] = first_infeasible<N>(a.lat, a.P.bmax, d, len);
+}
+
+template <int N, bool SIMPLE>
+__device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
+  using R = Rec<N>;
+  const int M = a.M, nip = a.do_ip ? 1 : 0;
+  const bool isip = q < nip;
+  const int row = q - nip;
+  const int len = isip ? M : M - row;
+  const int b0q = a.b0[q];
+  const int cnt = b0q < len ? b0q : len;
+  const double dlq = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[row];
+  const double INF = dinf();
+  double* gE = isip ? a.ipres : a.G + tri_u(row, row, M);
+  uint16_t* gB = isip ? a.ipb : a.bstar + tri_u(row, row, M);
+  if (!isip)
+    for (int kk = lane; kk < len; kk += 32) gE[kk] = INF;
+  else if (lane == 0)
+    gE[0] = INF;
+  __syncwarp();
+  bool num_ok = true;
+#pragma unroll
+  for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(a.P.prefix[n]);
+  for (int base = 0; base < cnt; base += 32) {
+    const int b = base + lane + 1;
+    bool alive[1] = {b <= cnt};
+    const bool al[1] = {b == b0q};
+    const int kmin = isip ? M - 1 : (al[0] ? b0q - 1 : b - 1);
+    double s[1][N], tot[1] = {0.0};
+    if (alive[0] && !al[0]) {
+      start_times<N>(a.lat, a.P.bmax, dlq, b, s[0]);
+    } else {
+#pragma unroll
+      for (int n = 0; n < N; ++n) s[0][n] = -1.0;
+    }
+    int off = 0;
+    for (int kk = 0; kk < len; ++kk) {
+      if (alive[0]) {
+        const int ri = isip ? a.rank[kk] : row + kk;
+        int sp[1] = {0};
+        const bool live[1] = {true};
+        eval_multi<N, 1, SIMPLE>(a.rec + (size_t)ri * R::SIZE, a.P, s, al, num_ok, live, tot, sp);
+        alive[0] = sp[0] >= 0;
+        off += (sp[0] >= 0 && sp[0] < N);
+      }
+      const bool cand = alive[0] && kk >= kmin && off <= b;
+      const unsigned long long key = (unsigned long long)__double_as_longlong(tot[0]);
+      const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+      const unsigned mh = __reduce_min_sync(kFull, cand ? khi : 0xffffffffu);
+      const bool hit = cand && khi == mh;
+      unsigned wm = __ballot_sync(kFull, hit);
+      if (__popc(wm) > 1) {
+        const unsigned ml = __reduce_min_sync(kFull, hit ? klo : 0xffffffffu);
+        wm = __ballot_sync(kFull, hit && klo == ml);
+      }
+      if (wm != 0u && lane == 31 - __clz(wm)) {
+        const int slot = isip ? 0 : kk;
+        if (tot[0] <= gE[slot]) {  // later passes carry larger b: they win ties
+          gE[slot] = tot[0];
+          gB[slot] = (uint16_t)(al[0] ? kk + 1 : b);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) large_grow(LargeArgs a) {
+  if (*a.status != INT_MAX) return;
+  const int nip = a.do_ip ? 1 : 0, Q = nip + (a.do_og ? a.M : 0);
+  const int q = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (q >= Q) return;
+  if (*a.simple)
+    grow_row<N, true>(a, q, threadIdx.x & 31);
+  else
+    grow_row<N, false>(a, q, threadIdx.x & 31);
+}
+
+// One CTA: DP, backtrack, stitch, outputs (and the IP-SSA outputs).
+template <int N>
+__global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
+  using R = Rec<N>;
+  extern __shared__ __align__(16) unsigned char smb[];
+  const int M = a.M, nip = a.do_ip ? 1 : 0;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  double* dls = reinterpret_cast<double*>(smb);
+  double* PM = dls + M;
+  int* gl = reinterpret_cast<int*>(PM + M);
+  int* gh = gl + M;
+  __shared__ double wred[32];
+  __shared__ int ired[32];
+  __shared__ int s_best, s_ng, s_st;
+  const double INF = dinf();
+  const ProfileConst& P = a.P;
+  const size_t base = a.base;
+  if (*a.status != INT_MAX) {  // Scenario::check failed: first failing user, first test
+    if (tid == 0) {
+      if (a.do_ip && a.ip.status) a.ip.status[a.k] = *a.status & 31;
+      if (a.do_og && a.og.status) a.og.status[a.k] = *a.status & 31;
+    }
+    return;
+  }
+  for (int x = tid; x < M; x += NT) dls[x] = a.dls[x];
+  __syncthreads();
+
+  // ------------------------------------------------------------- IP-SSA out
+  if (a.do_ip) {
+    const double ipE = a.ipres[0];
+    const int ipbv = a.ipb[0];
+    if (ipE == INF) {
+      if (tid == 0 && a.ip.status) a.ip.status[a.k] = COINFER_ST_INFEASIBLE;
+    } else {
+      const double l_ip = a.has_l_ip ? a.l_ip : dls[0];
+      const bool pipe = ipbv < a.b0[0];
+      double s[N];
+      if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipbv, s);
+      else
+#pragma unroll
+        for (int n = 0; n < N; ++n) s[n] = 0.0;
+      for (int m = tid; m < M; m += NT) {
+        const double* r = a.rec + (size_t)a.rank[m] * R::SIZE;
+        int sp;
+        double f;
+        choose<N>(r, P, s, pipe, sp, f);
+        if (a.ip.split) a.ip.split[base + m] = (uint8_t)sp;
+        if (a.ip.freq) a.ip.freq[base + m] = f;
+        if (a.ip.user_energy) a.ip.user_energy[base + m] = fold<N>(r, sp, f, 0.0);
+        a.spos[a.rank[m]] = sp;
+      }
+      __syncthreads();
+      if (a.ip.batch_size)
+        for (int n = 1 + tid; n <= N; n += NT) {
+          int c = 0;
+          for (int x = 0; x < M; ++x) c += a.spos[x] < n;
+          a.ip.batch_size[(size_t)a.k * N + n - 1] = c;
+        }
+      if (tid == 0) {
+        if (a.ip.status) a.ip.status[a.k] = COINFER_ST_OK;
+        if (a.ip.batch_bound) a.ip.batch_bound[a.k] = ipbv;
+        if (a.ip.pipeline_feasible) a.ip.pipeline_feasible[a.k] = pipe;
+        if (a.ip.energy) a.ip.energy[a.k] = ipE;
+      }
+    }
+    __syncthreads();
+  }
+  if (!a.do_og) return;
+
+  // ------------------------------------------------------------------ DP
+  for (int j = tid; j < M; j += NT) {  // S[0][j] = G[0][j]
+    a.St[tri_l(j, 0)] = a.G[tri_u(0, j, M)];
+    a.par[tri_l(j, 0)] = 0xffff;
+  }
+  __syncthreads();
+  for (int i = 1; i < M; ++i) {
+    // prefix minimum of the column S[.][i-1] (contiguous in St row i-1)
+    const double* col = a.St + tri_l(i - 1, 0);
+    const int per = (i + NT - 1) / NT;  // consecutive elements per thread
+    const int p0 = tid * per;
+    double run = INF;
+    for (int p = p0; p < p0 + per && p < i; ++p) {
+      const double v = col[p];
+      if (v < run) run = v;
+      PM[p] = run;
+    }
+    // exclusive block scan (min) of the per-thread minima
+    double x = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off && y < x) x = y;
+    }
+    if (lane == 31) wred[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      double w = lane < NW ? wred[lane] : INF;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(kFull, w, off);
+        if (lane >= off && y < w) w = y;
+      }
+      if (lane < NW) wred[lane] = w;
+    }
+    __syncthreads();
+    double carry = __shfl_up_sync(kFull, x, 1);
+    if (lane == 0) carry = INF;
+    if (warp > 0 && wred[warp - 1] < carry) carry = wred[warp - 1];
+    for (int p = p0; p < p0 + per && p < i; ++p)
+      if (carry < PM[p]) PM[p] = carry;
+    __syncthreads();
+    const double di = dls[i];
+    for (int j = i + tid; j < M; j += NT) {
+      const double g = a.G[tri_u(i, j, M)];
+      const double sl = a.sumlat[j - i + 1];
+      int lo = 0, hi = i;  // P = #prevs with groups_fit (offline_solvers.hpp:229-232)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__dadd_rn(dls[mid], sl) <= di) lo = mid + 1; else hi = mid;
+      }
+      double res = INF;
+      int pr = 0xffff;
+      if (g != INF && lo > 0) {
+        const double m = PM[lo - 1];
+        const double v = __dadd_rn(m, g);
+        if (m != INF && v < INF) {
+          int l2 = 0, h2 = lo - 1;  // first p with fl(PM[p] + g) <= v: the smallest prev
+          while (l2 < h2) {
+            const int mid = (l2 + h2) >> 1;
+            if (__dadd_rn(PM[mid], g) <= v) h2 = mid; else l2 = mid + 1;
+          }
+          res = v;
+          pr = l2;
+        }
+      }
+      a.St[tri_l(j, i)] = res;
+      a.par[tri_l(j, i)] = (uint16_t)pr;
+    }
+    __syncthreads();
+  }
+
+  // best_i: strict '<', smallest i (offline_solvers.hpp:332-334); S[i][M-1] = St row M-1
+  {
+    double bv = INF;
+    int bi = M;
+    for (int i = tid; i < M; i += NT) {
+      const double v = a.St[tri_l(M - 1, i)];
+      if (v < bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int off = 16; off; off >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, off);
+      const int oi = __shfl_xor_sync(kFull, bi, off);
+      if (ov < bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      wred[warp] = bv;
+      ired[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v = INF;
+      int b = M;
+      for (int w = 0; w < NW; ++w)
+        if (wred[w] < v || (wred[w] == v && ired[w] < b)) {
+          v = wred[w];
+          b = ired[w];
+        }
+      s_best = v == INF ? -1 : b;
+      s_st = COINFER_ST_OK;
+    }
+    __syncthreads();
+  }
+  const int best_i = s_best;
+  if (a.og.order)
+    for (int i = tid; i < M; i += NT) a.og.order[base + i] = a.order[i];
+
+  if (best_i < 0) {  // lc_solve fallback (offline_solvers.hpp:336-348)
+    for (int i = tid; i < M; i += NT)
+      if (a.rec[(size_t)i * R::SIZE + R::FEAS] == 0.0) s_st = COINFER_ST_INFEASIBLE;
+    __syncthreads();
+    if (s_st != COINFER_ST_OK) {
+      if (tid == 0 && a.og.status) a.og.status[a.k] = COINFER_ST_INFEASIBLE;
+      return;
+    }
+    for (int i = tid; i < M; i += NT) {
+      const double* r = a.rec + (size_t)i * R::SIZE;
+      const double fL = r[R::FL];
+      const double e = fold<N>(r, N, fL, 0.0);
+      const int m = a.order[i];
+      const size_t g = base + i;
+      if (a.og.group_lo) a.og.group_lo[g] = i;
+      if (a.og.group_size) a.og.group_size[g] = 1;
+      if (a.og.group_b) a.og.group_b[g] = 0;
+      if (a.og.group_deadline) a.og.group_deadline[g] = dls[i];
+      if (a.og.group_energy) a.og.group_energy[g] = e;
+      if (a.og.group_batch_size)
+        for (int n = 0; n < N; ++n) a.og.group_batch_size[g * N + n] = 0;
+      if (a.og.group_of_user) a.og.group_of_user[base + m] = i;
+      if (a.og.split) a.og.split[base + m] = (uint8_t)N;
+      if (a.og.freq) a.og.freq[base + m] = fL;
+      if (a.og.user_energy) a.og.user_energy[base + m] = e;
+    }
+    if (tid == 0) {
+      double total = 0.0;  // lc_solve folds users in original order
+      for (int m = 0; m < M; ++m) {
+        const double* r = a.rec + (size_t)a.rank[m] * R::SIZE;
+        total = fold<N>(r, N, r[R::FL], total);
+      }
+      if (a.og.status) a.og.status[a.k] = COINFER_ST_OK;
+      if (a.og.fallback) a.og.fallback[a.k] = 1;
+      if (a.og.energy) a.og.energy[a.k] = total;
+      if (a.og.n_groups) a.og.n_groups[a.k] = M;
+    }
+    return;
+  }
+
+  // backtrack (offline_solvers.hpp:350-360)
+  if (tid == 0) {
+    int ng = 0, i = best_i, j = M - 1;
+    while (true) {
+      gl[ng] = i;
+      gh[ng] = j;
+      ++ng;
+      if (i == 0) break;
+      const int prev = a.par[tri_l(j, i)];
+      j = i - 1;
+      i = prev;
+    }
+    for (int x = 0, y = ng - 1; x < y; ++x, --y) {
+      int t = gl[x];
+      gl[x] = gl[y];
+      gl[y] = t;
+      t = gh[x];
+      gh[x] = gh[y];
+      gh[y] = t;
+    }
+    s_ng = ng;
+  }
+  __syncthreads();
+  const int ng = s_ng;
+  for (int g = tid; g < ng; g += NT)
+    for (int x = gl[g]; x <= gh[g]; ++x) a.gid[x] = g;
+  __syncthreads();
+  // stitch: re-derive each chosen group's plan from its stored bound
+  for (int x = tid; x < M; x += NT) {
+    const int g = a.gid[x];
+    const int lo = gl[g], hi = gh[g];
+    const int bb = a.bstar[tri_u(lo, hi, M)];
+    const bool pipe = bb < a.b0[nip + lo];
+    double s[N];
+    if (pipe) start_times<N>(a.lat, P.bmax, dls[lo], bb, s);
+    else
+#pragma unroll
+      for (int n = 0; n < N; ++n) s[n] = 0.0;
+    const double* r = a.rec + (size_t)x * R::SIZE;
+    int sp;
+    double f;
+    choose<N>(r, P, s, pipe, sp, f);
+    a.spos[x] = sp;
+    a.fpos[x] = f;
+    const int m = a.order[x];
+    if (a.og.group_of_user) a.og.group_of_user[base + m] = g;
+    if (a.og.split) a.og.split[base + m] = (uint8_t)sp;
+    if (a.og.freq) a.og.freq[base + m] = f;
+    if (a.og.user_energy) a.og.user_energy[base + m] = fold<N>(r, sp, f, 0.0);
+  }
+  __syncthreads();
+  for (int g = tid; g < ng; g += NT) {
+    const int lo = gl[g], hi = gh[g];
+    double total = 0.0;
+    for (int x = lo; x <= hi; ++x) total = fold<N>(a.rec + (size_t)x * R::SIZE, a.spos[x], a.fpos[x], total);
+    a.genergy[g] = total;
+    const size_t gi = base + g;
+    if (a.og.group_lo) a.og.group_lo[gi] = lo;
+    if (a.og.group_size) a.og.group_size[gi] = hi - lo + 1;
+    if (a.og.group_b) a.og.group_b[gi] = a.bstar[tri_u(lo, hi, M)];
+    if (a.og.group_deadline) a.og.group_deadline[gi] = dls[lo];
+    if (a.og.group_energy) a.og.group_energy[gi] = total;
+    if (a.og.group_batch_size)
+      for (int n = 1; n <= N; ++n) {
+        int c = 0;
+        for (int x = lo; x <= hi; ++x) c += a.spos[x] < n;
+        a.og.group_batch_size[gi * N + n - 1] = c;
+      }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double e = 0.0;  // plan.energy: left fold of group energies (:385-386)
+    for (int g = 0; g < ng; ++g) e = __dadd_rn(e, a.genergy[g]);
+    if (a.og.status) a.og.status[a.k] = COINFER_ST_OK;
+    if (a.og.fallback) a.og.fallback[a.k] = 0;
+    if (a.og.energy) a.og.energy[a.k] = e;
+    if (a.og.n_groups) a.og.n_groups[a.k] = ng;
+  }
+}
+
+size_t large_ws_bytes(int M, int N) {
+  const size_t T = (size_t)M * (M + 1) / 2;
+  const size_t rec = (size_t)M * rec_size(N) * 8;
+  // G, St (fp64) + bstar, par (u16) + records + dls/sumlat/fpos/genergy + ints
+  return 16 * T + 4 * T + rec + 8 * ((size_t)M + 2) * 4 + 4 * ((size_t)M + 2) * 5 + 4096 + 64 * 16;
+}
+
+__global__ void large_init(LargeArgs a) {
+  // Scenario::check tests the table length before any user (core_model.hpp:86-87)
+  *a.status = a.P.bmax < a.M ? COINFER_ST_SHORT_TABLE : INT_MAX;
+  *a.simple = 1;
+}
+
+template <int N>
+static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
+  const int M = a.M, Q = (a.do_ip ? 1 : 0) + (a.do_og ? M : 0);
+  large_init<<<1, 1, 0, st>>>(a);
+  large_prep<N><<<(M + 256) / 256, 256, 0, st>>>(a);
+  large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
+  large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
+  const int smem = 8 * 2 * M + 4 * 2 * M;
+  cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  large_finish<N><<<1, 1024, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_large(const LargeArgs& a, cudaStream_t st) {
+#define CFB_CALL(n) return launch_large_n<n>(a, st)
+  CFB_DISPATCH_N(a.P.N, CFB_CALL)
+#undef CFB_CALL
+}
+
+}  // namespace cfb
