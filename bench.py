@@ -5,9 +5,10 @@ Workload (BASELINE.json configs[2], "C3"): an offline Monte Carlo sweep of
 1,000,000 independent instances x M=50 users, heavy DNN profile (N=4,
 profile_heavy(b_max=M)), deadlines U[0.25, 1.0]; every instance gets IP-SSA
 at its smallest deadline AND OG optimal grouping (the CLI's IPSSA+OG pair,
-coinfer_main.cpp:237-245).  Instances are sharded across ranks (contiguous
-ranges, no data-path collective); one NCCL all-reduce of summary statistics
-closes the job.
+coinfer_main.cpp:237-245).  Weak scaling: each rank owns 1M instances of one
+global instance stream (contiguous ranges, shard.py), solves them with no
+data-path collective, and one NCCL all-reduce of summary statistics closes
+the job.
 
   value  device-resident throughput: inputs already in HBM, one fused
          solve launch per step, CUDA events on the launching stream, max over
@@ -41,7 +42,8 @@ sys.path.insert(0, ROOT)
 METRIC = "IP-SSA+OG instances solved/sec (C3: M=50 users, heavy profile)"
 UNIT = "instances/s"
 WORKLOAD = ("C3: IP-SSA (l = min deadline) + OG per instance, 1M independent instances x "
-            "M=50 users, profile_heavy(b_max=50) N=4, deadlines U[0.25,1.0]")
+            "M=50 users per GPU (weak scaling: instance shards, no data-path collective), "
+            "profile_heavy(b_max=50) N=4, deadlines U[0.25,1.0]")
 IP_E2E_FIELDS = ["status", "batch_bound", "energy", "split"]
 OG_E2E_FIELDS = ["status", "energy", "n_groups", "group_of_user", "split"]
 
@@ -52,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n-inst", type=int, default=1_000_000)
+    ap.add_argument("--n-inst", type=int, default=1_000_000, help="instances per GPU")
     ap.add_argument("--M", type=int, default=50)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -65,22 +67,13 @@ def parse():
 # ----------------------------------------------------------------- inputs
 
 def make_inputs(args, rank, world):
-    from paper_2206_06304_b200 import profile_heavy, sample_batch
-    M = args.M
-    prof = profile_heavy(M)
-    lo = args.n_inst * rank // world
-    hi = args.n_inst * (rank + 1) // world
-    # one RNG stream per 4096-instance block keeps the data identical however
-    # the job is sharded
-    blocks = []
-    b0 = lo - lo % 4096
-    for start in range(b0, hi, 4096):
-        blk = sample_batch(4096, M, prof, 0.25, 1.0, seed=args.seed * 1_000_003 + start // 4096)
-        a, b = max(lo, start) - start, min(hi, start + 4096) - start
-        blocks.append({k: v[a:b] for k, v in blk.items()})
-    fields = ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline"]
-    users = {k: np.concatenate([blk[k] for blk in blocks], 0) for k in fields}
-    return prof, users, lo, hi
+    """This rank's instances: weak scaling, `--n-inst` instances per rank, drawn
+    per 4096-instance block keyed by the global block index (shard.py)."""
+    from paper_2206_06304_b200 import profile_heavy
+    from paper_2206_06304_b200.shard import make_instances, shard_range
+    prof = profile_heavy(args.M)
+    lo, hi = shard_range(args.n_inst, rank, world)
+    return prof, make_instances(prof, args.M, lo, hi, seed=args.seed), lo, hi
 
 
 def feasibility_thresholds(prof):
@@ -228,9 +221,9 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_inst": args.n_inst, "M": args.M},
+            "config": {"workload": WORKLOAD, "n_inst_per_gpu": args.n_inst, "M": args.M},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return 0
@@ -238,6 +231,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2206_06304_b200 import Engine
+    from paper_2206_06304_b200.shard import max_over_ranks, reduce_summary, summary_stats
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -254,11 +248,7 @@ def main():
             dist.barrier()
 
     def allmax(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks(x, dist if world > 1 else None, f"cuda:{local}")
 
     # ---------------- device-resident throughput (value) ----------------
     with torch.cuda.stream(stream):
@@ -282,18 +272,10 @@ def main():
         launches = eng.launches - l0
         ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = allmax(ms)
-    value = args.n_inst / (ms_max * 1e-3)
+    value = args.n_inst * world / (ms_max * 1e-3)
 
     # ---------------- NCCL reduce of summary statistics ----------------
-    ok = (ip["status"] == 0) & (og["status"] == 0)
-    stats = torch.stack([
-        torch.where(ok, ip["energy"], 0.0).sum(), torch.where(ok, og["energy"], 0.0).sum(),
-        og["n_groups"].to(torch.float64).sum(), og["fallback"].to(torch.float64).sum(),
-        (~ok).to(torch.float64).sum(),
-        (og["split"].to(torch.float64) * (1 + torch.arange(args.M, device=og["split"].device))).sum()])
-    if world > 1:
-        dist.all_reduce(stats)
-    stats = stats.cpu().tolist()
+    summary = reduce_summary(summary_stats(torch, ip, og), dist if world > 1 else None)
 
     # ---------------- roofline (fp64 pipe) ----------------
     w_og, w_ip = work_model(prof, users)
@@ -345,16 +327,15 @@ def main():
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (sample_scenario distribution, numpy RNG, fixed seed)",
-            "config": {"workload": WORKLOAD, "n_inst": args.n_inst, "M": args.M, "N": prof.N,
+            "config": {"workload": WORKLOAD, "n_inst_per_gpu": args.n_inst,
+                       "n_inst_total": args.n_inst * world, "M": args.M, "N": prof.N,
                        "parallelism": f"instance shards x{world}",
                        "l2": "inputs 2.8 GB > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
-            "summary": {"ipssa_energy_sum": stats[0], "og_energy_sum": stats[1],
-                        "og_groups": stats[2], "og_fallbacks": stats[3],
-                        "failed_instances": stats[4], "og_split_checksum": stats[5]}}))
+            "summary": summary}))
     return 0
 
 
