@@ -22,6 +22,12 @@
  *                            run_offline_solver("IPSSA"/"OG")           tools/coinfer_main.cpp:237-245
  *   (per-user energies)   <- schedule_metrics(...).per_user_energy      offline_solvers.hpp:627-646
  *   (contract checks)     <- Scenario::check / DnnProfile::check        core_model.hpp:31-52,80-101
+ *   coinfer_ipssa_schedule / coinfer_og_schedule
+ *                         <- the Schedule built by try_fixed_batch / og + normalize
+ *                                                                       offline_solvers.hpp:155-185,357-386
+ *                                                                       schedule.hpp:93-113
+ *   coinfer_baseline_batch <- baseline(const Scenario&, BaselineMode)   offline_solvers.hpp:390-612
+ *   coinfer_best_partition <- best_partition / detail::local_only_choice offline_solvers.hpp:62-117
  *   coinfer_online_run    <- run_episode(OnlineEnv&, TimeWindowPolicy, horizon, seed)
  *                                                                       online_sim.hpp:131-249,312-371
  *
@@ -46,7 +52,7 @@
 extern "C" {
 #endif
 
-#define COINFER_ABI_VERSION 1
+#define COINFER_ABI_VERSION 2
 
 /* Call-level return codes. */
 #define COINFER_OK 0
@@ -147,6 +153,25 @@ typedef struct coinfer_og_out {
   int32_t* group_batch_size;/* [n_inst*M*N] realized batch size per sub-task per group */
 } coinfer_og_out;
 
+/* Schedule (schedule.hpp:26-36) in SoA form, normalised like
+   coinfer::normalize (schedule.hpp:93-113): batch ids 1..n_batches ordered by
+   (start time, sub-task).  x[(k*M + m)*N + n-1] is the placement of sub-task
+   n of user m (0 = local, COINFER kLocal); batch_start has capacity M*N per
+   instance; completion[(k*M + m)*(N+1) + n] = t_{m,n}. */
+typedef struct coinfer_schedule_out {
+  int32_t* x;           /* [n_inst*M*N]      */
+  int32_t* n_batches;   /* [n_inst]          */
+  double* batch_start;  /* [n_inst*M*N]      */
+  double* completion;   /* [n_inst*M*(N+1)]  */
+  double* freq;         /* [n_inst*M]        */
+} coinfer_schedule_out;
+
+/* Offline comparison baselines (BaselineMode, offline_solvers.hpp:390-612). */
+#define COINFER_BASELINE_LC 0       /* detail::lc_solve        :255-276 */
+#define COINFER_BASELINE_PS 1       /* detail::ps_solve        :404-487 */
+#define COINFER_BASELINE_FIFO 2     /* detail::fifo_solve      :489-555 */
+#define COINFER_BASELINE_IPSSA_NP 3 /* detail::ipssa_np_solve  :560-600 */
+
 /* Online slot driver: run_episode(OnlineEnv(scenario, ArrivalModel, solver,
    slot, seed), policy, horizon, seed) (online_sim.hpp:69-371), one episode
    per seed.  Policies: the fixed TimeWindowPolicy(window, l_high) and
@@ -233,6 +258,42 @@ int coinfer_og_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
 int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
                         const coinfer_users* users, coinfer_ipssa_out* ipssa,
                         coinfer_og_out* og);
+
+/* Schedule materialisation on the device (try_fixed_batch:155-185, the
+   og stitch :357-386 and normalize).  `solved` holds the decisions of an
+   earlier coinfer_ipssa_batch / coinfer_fixed_batch (status, batch_bound,
+   pipeline_feasible, split, freq, batch_size required) or coinfer_og_batch
+   call (status, fallback, n_groups, order, group_lo, group_size, group_b,
+   group_deadline, group_batch_size, split, freq required) on the same
+   inputs, in the same memory kind; deadline as in coinfer_ipssa_batch.
+   Instances whose status is not COINFER_ST_OK get n_batches 0 and untouched
+   rows.  Every member of `out` is required. */
+int coinfer_ipssa_schedule(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const double* deadline,
+                           const coinfer_ipssa_out* solved, coinfer_schedule_out* out);
+int coinfer_og_schedule(coinfer_ctx* ctx, const coinfer_profile* profile,
+                        const coinfer_users* users, const coinfer_og_out* solved,
+                        coinfer_schedule_out* out);
+
+/* baseline(sc, mode) (offline_solvers.hpp:602-612) for every instance:
+   SolveResult fields in `out` (batch_bound / pipeline_feasible are those of
+   the collapsed IP-SSA for IPSSA_NP, 0 / 1 otherwise), the schedule in
+   `sched` (optional; all members required when given).  Infeasible
+   instances get COINFER_ST_INFEASIBLE; the message per mode is
+   coinfer_status_message(status, "lc" | "ps" | "fifo" | "np"). */
+int coinfer_baseline_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, int32_t mode, coinfer_ipssa_out* out,
+                           coinfer_schedule_out* sched);
+
+/* best_partition (offline_solvers.hpp:83-117) for n independent (user,
+   start-time vector, deadline) queries, or detail::local_only_choice
+   (:62-75) when s is NULL.  Users are the n rows of `users` (n_inst = n,
+   M = 1); s is [n*N].  Outputs: PartitionChoice split / freq (NaN when
+   nothing runs locally) / energy (+inf when infeasible) / feasible.
+   Host memory only. */
+int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const double* s, int32_t* split,
+                           double* freq, double* energy, uint8_t* feasible);
 
 /* Run n_ep episodes; episode e simulates scenario e % users->n_inst (each a
    Scenario of users->M users; deadlines are only contract-checked) with

@@ -16,6 +16,9 @@
 //   ref_sample_scenario     coinfer::sample_scenario + profile_heavy/light
 //       (scenario_gen.hpp:113-216), seeded like the CLI (coinfer_main.cpp:47-50)
 //   ref_online_episode      run_episode(OnlineEnv, TimeWindowPolicy) (online_sim.hpp)
+//   ref_schedule_batch      the Schedule ip_ssa / og return, in the product's
+//       SoA schedule layout (coinfer_schedule_out)
+//   ref_baseline_batch      baseline(sc, BaselineMode) + its Schedule
 
 #include <atomic>
 #include <chrono>
@@ -163,9 +166,62 @@ int og_into(const Scenario& sc, int64_t k, int M, int N, coinfer_og_out* out) {
   return COINFER_ST_OK;
 }
 
+void write_schedule(const Schedule& s, int64_t k, int M, int N, coinfer_schedule_out* o) {
+  o->n_batches[k] = (int32_t)s.batch_start.size();
+  for (size_t i = 0; i < s.batch_start.size(); ++i) o->batch_start[(size_t)k * M * N + i] = s.batch_start[i];
+  for (int m = 0; m < M; ++m) {
+    o->freq[(size_t)k * M + m] = s.freq[m];
+    for (int n = 0; n < N; ++n) o->x[((size_t)k * M + m) * N + n] = (int32_t)s.x[m][n];
+    for (int n = 0; n <= N; ++n) o->completion[((size_t)k * M + m) * (N + 1) + n] = s.completion[m][n];
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+// kind 0: ip_ssa(sc, deadline[k] or the smallest deadline); kind 1: og(sc).
+// Returns per-instance statuses in status[k].
+int ref_schedule_batch(const coinfer_profile* p, const coinfer_users* u, const double* deadline,
+                       int kind, int32_t* status, coinfer_schedule_out* out) {
+  const DnnProfile prof = make_profile(p);
+  for (int64_t k = 0; k < u->n_inst; ++k) {
+    const Scenario sc = make_scenario(prof, u, k);
+    status[k] = guarded([&] {
+      if (kind == 0) {
+        double l = kInf;
+        for (double d : sc.deadline) l = std::min(l, d);
+        write_schedule(ip_ssa(sc, deadline ? deadline[k] : l).schedule, k, u->M, p->N, out);
+      } else {
+        write_schedule(og(sc).schedule, k, u->M, p->N, out);
+      }
+      return 0;
+    });
+  }
+  return COINFER_OK;
+}
+
+int ref_baseline_batch(const coinfer_profile* p, const coinfer_users* u, int mode,
+                       coinfer_ipssa_out* out, coinfer_schedule_out* sched) {
+  const DnnProfile prof = make_profile(p);
+  try {
+    prof.check();
+  } catch (const std::invalid_argument&) {
+    return COINFER_E_PROFILE;
+  }
+  for (int64_t k = 0; k < u->n_inst; ++k) {
+    const Scenario sc = make_scenario(prof, u, k);
+    const int st = guarded([&] {
+      const SolveResult r = baseline(sc, (BaselineMode)mode);
+      write_solve(r, sc, k, u->M, p->N, out);
+      if (sched) write_schedule(r.schedule, k, u->M, p->N, sched);
+      return 0;
+    });
+    if (out->status) out->status[k] = st;
+  }
+  return COINFER_OK;
+}
+
 
 int ref_ipssa_batch(const coinfer_profile* p, const coinfer_users* u, const double* deadline,
                     coinfer_ipssa_out* out) {

@@ -15,7 +15,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("COINFER_LIB") or os.path.join(_HERE, "libcoinfer_b200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 OK, E_ARG, E_PROFILE, E_CUDA, E_UNSUPPORTED = 0, 1, 2, 3, 4
 ST_OK, ST_INFEASIBLE = 0, 1
 ST_BAD_FREQ, ST_NEG_KAPPA, ST_BAD_RATE, ST_NEG_POWER = 10, 11, 12, 13
@@ -66,6 +66,19 @@ class OgOut(C.Structure):
     _fields_ = [(n, t) for n, t, _ in OG_FIELDS]
 
 
+SCHEDULE_FIELDS = [("x", _i32p, "KMN"), ("n_batches", _i32p, "K"),
+                   ("batch_start", _dp, "KMN"), ("completion", _dp, "KMN1"),
+                   ("freq", _dp, "KM")]
+
+
+class ScheduleOut(C.Structure):
+    _fields_ = [(n, t) for n, t, _ in SCHEDULE_FIELDS]
+
+
+BASELINE_LC, BASELINE_PS, BASELINE_FIFO, BASELINE_IPSSA_NP = 0, 1, 2, 3
+BASELINE_MODES = {"LC": BASELINE_LC, "PS": BASELINE_PS, "FIFO": BASELINE_FIFO,
+                  "IPSSA_NP": BASELINE_IPSSA_NP}
+
 ARRIVAL_BERNOULLI, ARRIVAL_IMMEDIATE = 0, 1
 SOLVER_IPSSA, SOLVER_OG = 0, 1
 POLICY_TW, POLICY_LOCAL = 0, 1
@@ -105,6 +118,15 @@ PRODUCT_SYMBOLS = {
                                    C.POINTER(OgOut)]),
     "coinfer_sweep_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                       C.POINTER(IpssaOut), C.POINTER(OgOut)]),
+    "coinfer_ipssa_schedule": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
+                                         C.POINTER(IpssaOut), C.POINTER(ScheduleOut)]),
+    "coinfer_og_schedule": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                      C.POINTER(OgOut), C.POINTER(ScheduleOut)]),
+    "coinfer_baseline_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                         C.c_int32, C.POINTER(IpssaOut),
+                                         C.POINTER(ScheduleOut)]),
+    "coinfer_best_partition": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
+                                         _i32p, _dp, _dp, _u8p]),
     "coinfer_online_run": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                      C.POINTER(OnlineCfg), C.POINTER(C.c_uint64), C.c_int64,
                                      C.POINTER(OnlineOut)]),

@@ -37,6 +37,9 @@ struct coinfer_ctx {
   // large-instance path workspace (G/S triangles etc.)
   unsigned char* big = nullptr;
   size_t big_cap = 0;
+  // schedule / baseline / partition calls: staging + scratch (baselines.cu)
+  unsigned char* aux = nullptr;
+  size_t aux_cap = 0;
 };
 
 namespace {
@@ -530,6 +533,246 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   return COINFER_OK;
 }
 
+// ------------------------------------------------ schedule / baseline calls
+
+int ensure_aux(coinfer_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->aux_cap) return COINFER_OK;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->aux) cudaFree(ctx->aux);
+  ctx->aux = nullptr;
+  ctx->aux_cap = 0;
+  cudaError_t e = cudaMalloc(&ctx->aux, bytes);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(aux workspace)");
+  ctx->aux_cap = bytes;
+  return COINFER_OK;
+}
+
+template <class T>
+void plan_in_mut(Stager& s, T*& p, size_t count) {
+  const T* q = p;
+  plan_in(s, q, count);
+  p = const_cast<T*>(q);
+}
+
+enum class Aux { MatIp, MatOg, Baseline };
+
+int check_users(coinfer_ctx* ctx, const coinfer_users* users) {
+  if (!users) return fail(ctx, COINFER_E_ARG, "users: null");
+  if (users->n_inst < 0 || users->M < 0) return fail(ctx, COINFER_E_ARG, "users: negative size");
+  if (users->mem != COINFER_MEM_HOST && users->mem != COINFER_MEM_DEVICE)
+    return fail(ctx, COINFER_E_ARG, "users: bad mem kind");
+  if (users->M > 0 && users->n_inst > 0 &&
+      (!users->f_min || !users->f_max || !users->kappa || !users->rate_up || !users->power_up ||
+       !users->arrival || !users->deadline))
+    return fail(ctx, COINFER_E_ARG, "users: null input array");
+  return COINFER_OK;
+}
+
+bool sched_complete(const coinfer_schedule_out* o) {
+  return o && o->x && o->n_batches && o->batch_start && o->completion && o->freq;
+}
+
+// Shared driver of coinfer_{ipssa,og}_schedule and coinfer_baseline_batch:
+// host batches are staged whole through ctx->aux; device batches run in place.
+int run_aux(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* users,
+            const double* deadline, Aux kind, int mode, coinfer_ipssa_out* ip,
+            const coinfer_og_out* og, coinfer_schedule_out* sch) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  int rc = check_users(ctx, users);
+  if (rc != COINFER_OK) return rc;
+  rc = check_profile(ctx, prof);
+  if (rc != COINFER_OK) return rc;
+  if (users->n_inst == 0) return COINFER_OK;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+
+  const size_t K = (size_t)users->n_inst, M = (size_t)users->M, N = (size_t)prof->N;
+  const bool host = users->mem == COINFER_MEM_HOST;
+  cfb::AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.P = make_const(prof);
+  a.n_inst = users->n_inst;
+  a.M = users->M;
+  a.mode = mode;
+  a.fmin = users->f_min;
+  a.fmax = users->f_max;
+  a.kappa = users->kappa;
+  a.ru = users->rate_up;
+  a.pu = users->power_up;
+  a.arr = users->arrival;
+  a.dl = users->deadline;
+  a.rd = users->rate_down;
+  a.pd = users->power_down;
+  a.l_ip = deadline;
+  if (kind == Aux::MatIp) {  // only the decision arrays the materialiser reads
+    a.ip.status = ip->status;
+    a.ip.batch_bound = ip->batch_bound;
+    a.ip.pipeline_feasible = ip->pipeline_feasible;
+    a.ip.split = ip->split;
+    a.ip.freq = ip->freq;
+    a.ip.batch_size = ip->batch_size;
+  } else if (kind == Aux::MatOg) {
+    a.og.status = og->status;
+    a.og.fallback = og->fallback;
+    a.og.n_groups = og->n_groups;
+    a.og.order = og->order;
+    a.og.split = og->split;
+    a.og.freq = og->freq;
+    a.og.group_lo = og->group_lo;
+    a.og.group_size = og->group_size;
+    a.og.group_b = og->group_b;
+    a.og.group_deadline = og->group_deadline;
+    a.og.group_batch_size = og->group_batch_size;
+  } else {
+    a.ip = *ip;
+  }
+  if (sch) a.sch = *sch;
+
+  Stager st{ctx};
+  if (host) {
+    plan_in(st, a.fmin, K * M);
+    plan_in(st, a.fmax, K * M);
+    plan_in(st, a.kappa, K * M);
+    plan_in(st, a.ru, K * M);
+    plan_in(st, a.pu, K * M);
+    plan_in(st, a.arr, K * M);
+    plan_in(st, a.dl, K * M);
+    plan_in(st, a.rd, K * M);
+    plan_in(st, a.pd, K * M);
+    plan_in(st, a.l_ip, K);
+    if (kind == Aux::MatIp) {
+      plan_in_mut(st, a.ip.status, K);
+      plan_in_mut(st, a.ip.batch_bound, K);
+      plan_in_mut(st, a.ip.pipeline_feasible, K);
+      plan_in_mut(st, a.ip.split, K * M);
+      plan_in_mut(st, a.ip.freq, K * M);
+      plan_in_mut(st, a.ip.batch_size, K * N);
+    } else if (kind == Aux::MatOg) {
+      plan_in_mut(st, a.og.status, K);
+      plan_in_mut(st, a.og.fallback, K);
+      plan_in_mut(st, a.og.n_groups, K);
+      plan_in_mut(st, a.og.order, K * M);
+      plan_in_mut(st, a.og.split, K * M);
+      plan_in_mut(st, a.og.freq, K * M);
+      plan_in_mut(st, a.og.group_lo, K * M);
+      plan_in_mut(st, a.og.group_size, K * M);
+      plan_in_mut(st, a.og.group_b, K * M);
+      plan_in_mut(st, a.og.group_deadline, K * M);
+      plan_in_mut(st, a.og.group_batch_size, K * M * N);
+    } else {
+      plan_ip_out(st, a.ip, K, M, N);
+    }
+    if (sch) {
+      plan_out(st, a.sch.x, K * M * N);
+      plan_out(st, a.sch.n_batches, K);
+      plan_out(st, a.sch.batch_start, K * M * N);
+      plan_out(st, a.sch.completion, K * M * (N + 1));
+      plan_out(st, a.sch.freq, K * M);
+    }
+  }
+  const size_t nlat = N * (size_t)prof->b_max;
+  const size_t lat_off = st.reserve(nlat * 8);
+  const int grid = cfb::aux_grid(users->n_inst);
+  a.scratch_per_thread = (cfb::aux_scratch_bytes((int)M, (int)N) + 255) & ~size_t(255);
+  const size_t scr_off = st.reserve((size_t)grid * 128 * a.scratch_per_thread);
+  const bool np = kind == Aux::Baseline && mode == COINFER_BASELINE_IPSSA_NP;
+  size_t f_st = 0, f_bb = 0, f_pf = 0, f_sp = 0, f_fr = 0, f_bs = 0;
+  if (np) {
+    f_st = st.reserve(4 * K);
+    f_bb = st.reserve(4 * K);
+    f_pf = st.reserve(K);
+    f_sp = st.reserve(K * M);
+    f_fr = st.reserve(8 * K * M);
+    f_bs = st.reserve(4 * K);
+  }
+  rc = ensure_aux(ctx, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->aux;
+  cudaStream_t sp = ctx->stream;
+  if (host) {
+    patch(b, a.fmin);
+    patch(b, a.fmax);
+    patch(b, a.kappa);
+    patch(b, a.ru);
+    patch(b, a.pu);
+    patch(b, a.arr);
+    patch(b, a.dl);
+    patch(b, a.rd);
+    patch(b, a.pd);
+    patch(b, a.l_ip);
+    patch_ip_out(b, a.ip);
+    patch_og_out(b, a.og);
+    if (sch) {
+      patch(b, a.sch.x);
+      patch(b, a.sch.n_batches);
+      patch(b, a.sch.batch_start);
+      patch(b, a.sch.completion);
+      patch(b, a.sch.freq);
+    }
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+    }
+  }
+  a.lat = reinterpret_cast<const double*>(b + lat_off);
+  e = cudaMemcpyAsync(b + lat_off, prof->latency, nlat * 8, cudaMemcpyHostToDevice, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D latency");
+  a.scratch = b + scr_off;
+
+  if (np) {
+    // the collapsed one-sub-task profile (ipssa_np_solve:563-569): work =
+    // total_work, bits = {B_0, B_N}, F(b) = sum_latency(b) (a left fold)
+    std::vector<double> fw(1, a.P.prefix[N]), fb{prof->data_bits[0], prof->data_bits[N]};
+    std::vector<double> fl((size_t)prof->b_max);
+    for (int bb = 0; bb < prof->b_max; ++bb) {
+      double t = 0.0;
+      for (size_t n = 0; n < N; ++n) t += prof->latency[n * prof->b_max + bb];
+      fl[bb] = t;
+    }
+    coinfer_profile flat{1, prof->b_max, fw.data(), fb.data(), fl.data()};
+    coinfer_users du = *users;
+    du.mem = COINFER_MEM_DEVICE;
+    du.f_min = a.fmin;
+    du.f_max = a.fmax;
+    du.kappa = a.kappa;
+    du.rate_up = a.ru;
+    du.power_up = a.pu;
+    du.arrival = a.arr;
+    du.deadline = a.dl;
+    du.rate_down = a.rd;
+    du.power_down = a.pd;
+    std::memset(&a.flat, 0, sizeof a.flat);
+    a.flat.status = reinterpret_cast<int32_t*>(b + f_st);
+    a.flat.batch_bound = reinterpret_cast<int32_t*>(b + f_bb);
+    a.flat.pipeline_feasible = b + f_pf;
+    a.flat.split = b + f_sp;
+    a.flat.freq = reinterpret_cast<double*>(b + f_fr);
+    a.flat.batch_size = reinterpret_cast<int32_t*>(b + f_bs);
+    rc = run(ctx, &flat, &du, nullptr, nullptr, &a.flat, nullptr, Mode::Solve);
+    if (rc != COINFER_OK) return rc;
+  }
+  if (kind == Aux::MatIp)
+    e = cfb::launch_materialize_ip(a, sp);
+  else if (kind == Aux::MatOg)
+    e = cfb::launch_materialize_og(a, sp);
+  else
+    e = cfb::launch_baseline(a, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+  if (host) {
+    for (const auto& x : st.back) {
+      e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+    }
+  }
+  // the latency table was copied from pageable host memory the caller owns;
+  // host calls are synchronous anyway
+  e = cudaStreamSynchronize(sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "aux kernel");
+  return COINFER_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -556,6 +799,7 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_lat) cudaFree(ctx->d_lat);
   if (ctx->big) cudaFree(ctx->big);
+  if (ctx->aux) cudaFree(ctx->aux);
   for (int i = 0; i < 2; ++i) {
     if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);
     if (ctx->ws2[i]) cudaFree(ctx->ws2[i]);
@@ -603,6 +847,8 @@ const char* coinfer_status_message(int32_t status, const char* solver) {
     case COINFER_ST_INFEASIBLE:
       if (s == "og") return "baseline: user cannot meet the deadline locally";
       if (s == "fixed") return "fixed_batch_schedule: user cannot meet the deadline";
+      if (s == "lc") return "baseline: user cannot meet the deadline locally";
+      if (s == "ps" || s == "fifo") return "baseline: user cannot meet the deadline";
       return "ip_ssa: no batch bound admits every user";
     case COINFER_ST_BAD_FREQ: return "scenario: bad frequency range";
     case COINFER_ST_NEG_KAPPA: return "scenario: negative kappa";
@@ -796,6 +1042,112 @@ int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const 
                         coinfer_ipssa_out* ipssa, coinfer_og_out* og) {
   if (!ipssa && !og) return fail(ctx, COINFER_E_ARG, "sweep: no output requested");
   return run(ctx, profile, users, nullptr, nullptr, ipssa, og, Mode::Solve);
+}
+
+int coinfer_ipssa_schedule(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const double* deadline,
+                           const coinfer_ipssa_out* solved, coinfer_schedule_out* out) {
+  if (!solved || !solved->status || !solved->batch_bound || !solved->pipeline_feasible ||
+      !solved->split || !solved->freq || !solved->batch_size)
+    return fail(ctx, COINFER_E_ARG, "ipssa_schedule: decision arrays missing");
+  if (!sched_complete(out)) return fail(ctx, COINFER_E_ARG, "ipssa_schedule: schedule arrays missing");
+  coinfer_ipssa_out in = *solved;
+  return run_aux(ctx, profile, users, deadline, Aux::MatIp, 0, &in, nullptr, out);
+}
+
+int coinfer_og_schedule(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                        const coinfer_og_out* solved, coinfer_schedule_out* out) {
+  if (!solved || !solved->status || !solved->fallback || !solved->n_groups || !solved->order ||
+      !solved->split || !solved->freq || !solved->group_lo || !solved->group_size ||
+      !solved->group_b || !solved->group_deadline || !solved->group_batch_size)
+    return fail(ctx, COINFER_E_ARG, "og_schedule: decision arrays missing");
+  if (!sched_complete(out)) return fail(ctx, COINFER_E_ARG, "og_schedule: schedule arrays missing");
+  return run_aux(ctx, profile, users, nullptr, Aux::MatOg, 0, nullptr, solved, out);
+}
+
+int coinfer_baseline_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, int32_t mode, coinfer_ipssa_out* out,
+                           coinfer_schedule_out* sched) {
+  if (!out) return fail(ctx, COINFER_E_ARG, "baseline: null output");
+  if (mode < COINFER_BASELINE_LC || mode > COINFER_BASELINE_IPSSA_NP)
+    return fail(ctx, COINFER_E_ARG, "baseline: unknown mode");
+  if (sched && !sched_complete(sched))
+    return fail(ctx, COINFER_E_ARG, "baseline: schedule arrays missing");
+  return run_aux(ctx, profile, users, nullptr, Aux::Baseline, mode, out, nullptr, sched);
+}
+
+int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const double* s, int32_t* split,
+                           double* freq, double* energy, uint8_t* feasible) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  int rc = check_users(ctx, users);
+  if (rc != COINFER_OK) return rc;
+  if (users->mem != COINFER_MEM_HOST || users->M != 1)
+    return fail(ctx, COINFER_E_ARG, "best_partition: host memory, one user per query");
+  if (!split || !freq || !energy || !feasible) return fail(ctx, COINFER_E_ARG, "best_partition: null output");
+  rc = check_profile(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+  if (users->n_inst == 0) return COINFER_OK;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  const size_t K = (size_t)users->n_inst, N = (size_t)profile->N;
+  cfb::AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.P = make_const(profile);
+  a.n_inst = users->n_inst;
+  a.M = 1;
+  a.fmin = users->f_min;
+  a.fmax = users->f_max;
+  a.kappa = users->kappa;
+  a.ru = users->rate_up;
+  a.pu = users->power_up;
+  a.arr = users->arrival;
+  a.dl = users->deadline;
+  Stager st{ctx};
+  plan_in(st, a.fmin, K);
+  plan_in(st, a.fmax, K);
+  plan_in(st, a.kappa, K);
+  plan_in(st, a.ru, K);
+  plan_in(st, a.pu, K);
+  plan_in(st, a.arr, K);
+  plan_in(st, a.dl, K);
+  const double* sd = s;
+  plan_in(st, sd, K * N);
+  plan_out(st, split, K);
+  plan_out(st, freq, K);
+  plan_out(st, energy, K);
+  plan_out(st, feasible, K);
+  rc = ensure_aux(ctx, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->aux;
+  cudaStream_t sp = ctx->stream;
+  patch(b, a.fmin);
+  patch(b, a.fmax);
+  patch(b, a.kappa);
+  patch(b, a.ru);
+  patch(b, a.pu);
+  patch(b, a.arr);
+  patch(b, a.dl);
+  patch(b, sd);
+  patch(b, split);
+  patch(b, freq);
+  patch(b, energy);
+  patch(b, feasible);
+  for (const auto& x : st.in) {
+    e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+  }
+  e = cfb::launch_partition(a, sd, split, freq, energy, feasible, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+  for (const auto& x : st.back) {
+    e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+  }
+  e = cudaStreamSynchronize(sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "best_partition");
+  return COINFER_OK;
 }
 
 }  // extern "C"

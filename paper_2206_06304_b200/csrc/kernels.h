@@ -81,6 +81,32 @@ struct LargeArgs {
   coinfer_og_out og;
 };
 
+// Arguments of the schedule-materialisation and baseline kernels
+// (baselines.cu): one thread per instance, all pointers device memory.
+struct AuxArgs {
+  ProfileConst P;
+  const double* lat;  // the caller's profile table [N*bmax]
+  int64_t n_inst;
+  int M;
+  const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl, *rd, *pd;
+  const double* l_ip;       // IP-SSA / fixed deadline per instance, NULL = smallest user deadline
+  coinfer_ipssa_out ip;     // baseline results, or the IP-SSA decisions to materialise
+  coinfer_og_out og;        // the OG decisions to materialise
+  coinfer_ipssa_out flat;   // IPSSA_NP: the collapsed-profile IP-SSA decisions
+  coinfer_schedule_out sch; // Schedule (x, batch_start, completion, freq)
+  int mode;                 // COINFER_BASELINE_*
+  unsigned char* scratch;   // per-thread scratch, scratch_per_thread bytes each
+  size_t scratch_per_thread;
+};
+
+size_t aux_scratch_bytes(int M, int N);
+int aux_grid(int64_t n_inst);
+cudaError_t launch_materialize_ip(const AuxArgs& a, cudaStream_t st);
+cudaError_t launch_materialize_og(const AuxArgs& a, cudaStream_t st);
+cudaError_t launch_baseline(const AuxArgs& a, cudaStream_t st);
+cudaError_t launch_partition(const AuxArgs& a, const double* s, int32_t* split, double* freq,
+                             double* energy, uint8_t* feasible, cudaStream_t st);
+
 int small_smem_bytes(int M, int N, int W);
 int online_smem_bytes(int M, int N);
 size_t large_ws_bytes(int M, int N);

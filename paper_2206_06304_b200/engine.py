@@ -120,9 +120,9 @@ class Packed:
 
     def _alloc(self, fields, struct, only, mem, device):
         dims = {"K": self.K, "KM": self.K * self.M, "KN": self.K * self.N,
-                "KMN": self.K * self.M * self.N}
+                "KMN": self.K * self.M * self.N, "KMN1": self.K * self.M * (self.N + 1)}
         shapes = {"K": (self.K,), "KM": (self.K, self.M), "KN": (self.K, self.N),
-                  "KMN": (self.K, self.M, self.N)}
+                  "KMN": (self.K, self.M, self.N), "KMN1": (self.K, self.M, self.N + 1)}
         arrays, ptrs = {}, []
         for name, ctype, dim in fields:
             k = _kind(ctype)
@@ -245,6 +245,68 @@ class Engine:
         self._check(self.lib.coinfer_og_batch(self.ctx, C.byref(pk.profile), C.byref(pk.users),
                                               C.byref(pk.out_og)))
         return Packed.arrays(pk.out_og)
+
+    def _schedule_out(self, pk, mem):
+        return pk._alloc(_abi.SCHEDULE_FIELDS, _abi.ScheduleOut, None, mem, f"cuda:{self.device}")
+
+    @staticmethod
+    def _as_struct(struct, fields, arrays):
+        ptrs = []
+        for name, ctype, _ in fields:
+            a = arrays.get(name)
+            ptrs.append(C.cast(None, ctype) if a is None else _ptr(a, _CT[_kind(ctype)]))
+        return struct(*ptrs)
+
+    def ipssa_schedule(self, profile, users: Dict, solved: Dict, deadline=None):
+        """The Schedule of IP-SSA / fixed-bound decisions `solved` (as returned by
+        ipssa() / fixed()), built and normalised on the device
+        (try_fixed_batch:155-185, normalize)."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, False, False)
+        d = self._aux(deadline, mem, np.float64)
+        so = self._schedule_out(pk, mem)
+        ins = self._as_struct(_abi.IpssaOut, _abi.IPSSA_FIELDS, solved)
+        self._check(self.lib.coinfer_ipssa_schedule(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                    _ptr(d, C.c_double), C.byref(ins), C.byref(so)))
+        return Packed.arrays(so)
+
+    def og_schedule(self, profile, users: Dict, solved: Dict):
+        """The Schedule of an OG plan (og:357-386 + normalize), on the device."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, False, False)
+        so = self._schedule_out(pk, mem)
+        ins = self._as_struct(_abi.OgOut, _abi.OG_FIELDS, solved)
+        self._check(self.lib.coinfer_og_schedule(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                 C.byref(ins), C.byref(so)))
+        return Packed.arrays(so)
+
+    def baseline(self, profile, users: Dict, mode: str, schedule: bool = True, fields=None):
+        """baseline(sc, BaselineMode) for every instance (offline_solvers.hpp:390-612):
+        mode in LC / PS / FIFO / IPSSA_NP.  Returns (SolveResult arrays,
+        schedule arrays or None)."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, True, False, f"cuda:{self.device}", ip_fields=fields)
+        so = self._schedule_out(pk, mem) if schedule else None
+        self._check(self.lib.coinfer_baseline_batch(
+            self.ctx, C.byref(pk.profile), C.byref(pk.users), _abi.BASELINE_MODES[mode],
+            C.byref(pk.out_ip), C.byref(so) if so is not None else None))
+        return Packed.arrays(pk.out_ip), (Packed.arrays(so) if so is not None else None)
+
+    def best_partition(self, profile, users: Dict, s=None):
+        """best_partition (s: [n, N] start times) or local_only_choice (s None)
+        for n single-user queries (users fields of shape (n, 1)); host memory."""
+        pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+        n = pk.K
+        split = np.zeros(n, np.int32)
+        freq, energy = np.zeros(n), np.zeros(n)
+        feas = np.zeros(n, np.uint8)
+        sa = None if s is None else np.ascontiguousarray(s, dtype=np.float64)
+        self.lib.coinfer_ctx_reset_stream(self.ctx)
+        self._check(self.lib.coinfer_best_partition(
+            self.ctx, C.byref(pk.profile), C.byref(pk.users), _ptr(sa, C.c_double),
+            _ptr(split, C.c_int32), _ptr(freq, C.c_double), _ptr(energy, C.c_double),
+            _ptr(feas, C.c_uint8)))
+        return dict(split=split, freq=freq, energy=energy, feasible=feas)
 
     def sweep(self, profile, users: Dict, ipssa=True, og=True, ip_fields=None, og_fields=None,
               pinned=False):

@@ -41,6 +41,8 @@ REF_SYMBOLS = {
     "ref_oracle_grouping": (C.c_double, [_P, _U, C.c_int64, _i32p]),
     "ref_sweep_threads": (C.c_double, [_P, _U, C.POINTER(C.c_int64), C.c_int64, C.c_int, C.c_int,
                                        C.c_int, _dp, _dp]),
+    "ref_schedule_batch": (C.c_int, [_P, _U, _dp, C.c_int, _i32p, C.POINTER(_abi.ScheduleOut)]),
+    "ref_baseline_batch": (C.c_int, [_P, _U, C.c_int, _IO, C.POINTER(_abi.ScheduleOut)]),
     "ref_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ref_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
     "ref_rng_new": (C.c_void_p, [C.c_uint64]),
@@ -120,6 +122,49 @@ def ref_og(profile, users):
     pk = Packed(profile, users, _abi.MEM_HOST, False, True)
     assert ref().ref_og_batch(C.byref(pk.profile), C.byref(pk.users), C.byref(pk.out_og)) == 0
     return Packed.arrays(pk.out_og)
+
+
+def _sched_struct(pk):
+    return pk._alloc(_abi.SCHEDULE_FIELDS, _abi.ScheduleOut, None, _abi.MEM_HOST, None)
+
+
+def ref_schedule(profile, users, kind, deadline=None):
+    """The Schedule the reference's ip_ssa (kind "ipssa") or og returns, SoA."""
+    pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+    so = _sched_struct(pk)
+    st = np.zeros(pk.K, np.int32)
+    d = None if deadline is None else np.ascontiguousarray(deadline, dtype=np.float64)
+    assert ref().ref_schedule_batch(C.byref(pk.profile), C.byref(pk.users),
+                                    d.ctypes.data_as(_dp) if d is not None else None,
+                                    0 if kind == "ipssa" else 1, st.ctypes.data_as(_i32p),
+                                    C.byref(so)) == 0
+    out = Packed.arrays(so)
+    out["status"] = st
+    return out
+
+
+def ref_baseline(profile, users, mode):
+    """baseline(sc, BaselineMode[mode]) through the reference: (SolveResult, Schedule)."""
+    pk = Packed(profile, users, _abi.MEM_HOST, True, False)
+    so = _sched_struct(pk)
+    rc = ref().ref_baseline_batch(C.byref(pk.profile), C.byref(pk.users),
+                                  _abi.BASELINE_MODES[mode], C.byref(pk.out_ip), C.byref(so))
+    assert rc == 0, rc
+    return Packed.arrays(pk.out_ip), Packed.arrays(so)
+
+
+def assert_same_schedule(a: dict, b: dict, status, where=""):
+    """Schedules of the solved instances (status 0) equal bit for bit."""
+    ok = np.asarray(_to_np(status)) == 0
+    nb_a, nb_b = _to_np(a["n_batches"]), _to_np(b["n_batches"])
+    np.testing.assert_array_equal(nb_a[ok], nb_b[ok], err_msg=f"{where} n_batches")
+    for key in ("x", "completion", "freq"):
+        np.testing.assert_array_equal(_to_np(a[key])[ok], _to_np(b[key])[ok], err_msg=f"{where} {key}")
+    bs_a, bs_b = _to_np(a["batch_start"]), _to_np(b["batch_start"])
+    for k in np.nonzero(ok)[0]:
+        n = int(nb_a[k])
+        np.testing.assert_array_equal(bs_a[k].reshape(-1)[:n], bs_b[k].reshape(-1)[:n],
+                                      err_msg=f"{where} batch_start[{k}]")
 
 
 # --------------------------------------------------------------- comparison

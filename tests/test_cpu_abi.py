@@ -34,6 +34,11 @@ def test_abi_version_and_messages():
         "baseline: user cannot meet the deadline locally"
     assert lib.coinfer_status_message(_abi.ST_BAD_RATE, b"og").decode() == \
         "scenario: rates must be positive"
+    assert lib.coinfer_status_message(_abi.ST_INFEASIBLE, b"lc").decode() == \
+        "baseline: user cannot meet the deadline locally"
+    for m in (b"ps", b"fifo"):
+        assert lib.coinfer_status_message(_abi.ST_INFEASIBLE, m).decode() == \
+            "baseline: user cannot meet the deadline"
 
 
 def test_struct_layout_matches_header():
@@ -42,6 +47,7 @@ def test_struct_layout_matches_header():
     assert C.sizeof(_abi.Users) == 16 + 9 * 8
     assert C.sizeof(_abi.IpssaOut) == 8 * 8
     assert C.sizeof(_abi.OgOut) == 15 * 8
+    assert C.sizeof(_abi.ScheduleOut) == 5 * 8
 
 
 def test_no_context_without_gpu_is_loud():
