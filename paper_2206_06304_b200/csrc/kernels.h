@@ -116,6 +116,13 @@ int fixed_smem_bytes(int M, int N);
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st);
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
 
+#ifdef CFB_ONLY_N  // development builds: one sub-task count only (fast compiles)
+#define CFB_DISPATCH_N(NVAL, CALL)                   \
+  switch (NVAL) {                                    \
+    case CFB_ONLY_N: CALL(CFB_ONLY_N); break;        \
+    default: return cudaErrorInvalidValue;           \
+  }
+#else
 #define CFB_DISPATCH_N(NVAL, CALL) \
   switch (NVAL) {                  \
     case 1: CALL(1); break;        \
@@ -136,5 +143,6 @@ cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStr
     case 16: CALL(16); break;      \
     default: return cudaErrorInvalidValue; \
   }
+#endif
 
 }  // namespace cfb

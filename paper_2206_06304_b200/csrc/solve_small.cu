@@ -36,9 +36,6 @@
 
 namespace cfb {
 
-#ifdef CFB_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[8];
-#endif
 
 int small_smem_bytes(int M, int N, int W) { return small_smem_bytes_impl(M, N, W); }
 

@@ -162,13 +162,15 @@ def test_best_partition_queries(engine):
     assert abs(r["energy"][0] - (3.0 / 49.0 + 0.02)) < 1e-12
     q0 = dict(q, kappa=np.zeros((1, 1)), power_up=np.zeros((1, 1)))
     r = engine.best_partition(prof, q0, s)
-    assert r["split"][0] == 2 and r["energy"][0] == 0.0 and r["freq"][0] == 0.2
+    assert r["split"][0] == 2 and r["energy"][0] == 0.0
+    assert abs(r["freq"][0] - 0.2) <= 4 * np.spacing(0.2)  # EXPECT_DOUBLE_EQ
     r = engine.best_partition(prof, dict(q, f_min=np.full((1, 1), 0.5)), s)
     assert r["freq"][0] >= 0.5
     r = engine.best_partition(prof, dict(q, deadline=np.full((1, 1), -1.0)), np.array([[-1.0, -1.0]]))
     assert r["feasible"][0] == 0 and np.isinf(r["energy"][0]) and np.isnan(r["freq"][0])
     r = engine.best_partition(prof, q, None)  # local_only_choice at the user's deadline
-    assert r["split"][0] == 2 and r["freq"][0] == 0.2 and r["feasible"][0] == 1
+    assert r["split"][0] == 2 and r["feasible"][0] == 1
+    assert abs(r["freq"][0] - 0.2) <= 4 * np.spacing(0.2)
     # split 0: nothing local, freq NaN
     r = engine.best_partition(prof, dict(q, rate_up=np.full((1, 1), 1e9)), np.array([[0.08, 0.09]]))
     assert r["split"][0] in (0, 1, 2)
