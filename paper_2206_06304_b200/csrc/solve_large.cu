@@ -45,7 +45,8 @@ __global__ void large_prep(LargeArgs a) {
     const int code = check_user(a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], rd, a.pu[m], pd,
                                 a.arr[m], a.dl[m]);
     if (code != COINFER_ST_OK && *a.status != COINFER_ST_SHORT_TABLE) atomicMin(a.status, m * 32 + code);
-    if (!(a.arr[m] == 0.0 && a.fmin[m] == 0.0)) atomicAnd(a.simple, 0);
+    // SIMPLE path conditions (solve_core.cuh, device_common.cuh: fast_div_*)
+    if (!(a.arr[m] == 0.0 && a.fmin[m] == 0.0 && fast_div_deadline(a.dl[m]))) atomicAnd(a.simple, 0);
     const double d = a.dl[m];
     int r = 0;
     for (int o = 0; o < M; ++o) {  // stable rank by (deadline, id), offline_solvers.hpp:292-296
@@ -466,7 +467,7 @@ size_t large_ws_bytes(int M, int N) {
 __global__ void large_init(LargeArgs a) {
   // Scenario::check tests the table length before any user (core_model.hpp:86-87)
   *a.status = a.P.bmax < a.M ? COINFER_ST_SHORT_TABLE : INT_MAX;
-  *a.simple = 1;
+  *a.simple = fast_div_profile(a.P) && (!a.do_ip || !a.has_l_ip || fast_div_deadline(a.l_ip)) ? 1 : 0;
 }
 
 template <int N>
