@@ -13,9 +13,9 @@ namespace cfb {
 // Byte offsets of the fused kernel's shared-memory regions; computed on the
 // host once per launch so the kernel reads them from the constant bank.
 struct SmemLayout {
-  int rec, tri, dls, sumlat, headE, fsc;
-  int rowoff, b0, order, rank, gid, glo, ghi, headq, headlen, tpre, misc;
-  int headb, bstar, parent, spsc, ipb;
+  int rec, tri, dls, sumlat, ipe, fsc;
+  int rowoff, b0, order, rank, gid, glo, ghi, gitem, gbest, misc;
+  int pfit, argpm, parent, spsc, ipb;
   int total;
 };
 
