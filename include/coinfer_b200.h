@@ -27,6 +27,7 @@
  *                                                                       offline_solvers.hpp:155-185,357-386
  *                                                                       schedule.hpp:93-113
  *   coinfer_baseline_batch <- baseline(const Scenario&, BaselineMode)   offline_solvers.hpp:390-612
+ *   coinfer_validate_batch <- validate(const Schedule&, const Scenario&, double) schedule.hpp:139-209
  *   coinfer_best_partition <- best_partition / detail::local_only_choice offline_solvers.hpp:62-117
  *   coinfer_online_run    <- run_episode(OnlineEnv&, TimeWindowPolicy, horizon, seed)
  *                                                                       online_sim.hpp:131-249,312-371
@@ -294,6 +295,26 @@ int coinfer_baseline_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
 int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,
                            const coinfer_users* users, const double* s, int32_t* split,
                            double* freq, double* energy, uint8_t* feasible);
+
+/* validate(schedule, scenario, tol) (schedule.hpp:139-209) for every
+   instance, as violation counts per constraint id (the reference returns
+   the list; here one row of counts per instance, in this order):
+     C7-batchsize, C8-samesubtask, C9-batchready, C11-occupancy,
+     C12-precedence, C15-deadline, C17-initial.
+   `sched` is a coinfer_schedule_out as produced by the solvers (x,
+   n_batches, batch_start, completion, freq; same memory kind as the users;
+   rate_down / power_down used when given, else rate_up / power_up).
+   status[k]: COINFER_ST_OK, COINFER_ST_BAD_BATCH_ID ("schedule: batch id
+   beyond start-time table", invalid_argument), COINFER_ST_BOUND_PAST_TABLE
+   (a batch larger than the table, out_of_range) or COINFER_ST_NONPOS_FREQ
+   (local_latency with f <= 0, domain_error).  min_slack[k] (optional) is
+   the most negative slack found (0 if none). */
+#define COINFER_N_CONSTRAINTS 7
+#define COINFER_ST_BAD_BATCH_ID 19
+#define COINFER_ST_NONPOS_FREQ 23
+int coinfer_validate_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const coinfer_schedule_out* sched,
+                           double tol, int32_t* status, int32_t* counts, double* min_slack);
 
 /* Run n_ep episodes; episode e simulates scenario e % users->n_inst (each a
    Scenario of users->M users; deadlines are only contract-checked) with

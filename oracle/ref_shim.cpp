@@ -19,6 +19,7 @@
 //   ref_schedule_batch      the Schedule ip_ssa / og return, in the product's
 //       SoA schedule layout (coinfer_schedule_out)
 //   ref_baseline_batch      baseline(sc, BaselineMode) + its Schedule
+//   ref_validate_batch      validate(Schedule, Scenario, tol) as counts per constraint id
 
 #include <atomic>
 #include <chrono>
@@ -197,6 +198,46 @@ int ref_schedule_batch(const coinfer_profile* p, const coinfer_users* u, const d
       }
       return 0;
     });
+  }
+  return COINFER_OK;
+}
+
+int ref_validate_batch(const coinfer_profile* p, const coinfer_users* u,
+                       const coinfer_schedule_out* sc_in, double tol, int32_t* status,
+                       int32_t* counts, double* min_slack) {
+  static const char* ids[COINFER_N_CONSTRAINTS] = {"C7-batchsize", "C8-samesubtask", "C9-batchready",
+                                                   "C11-occupancy", "C12-precedence", "C15-deadline",
+                                                   "C17-initial"};
+  const DnnProfile prof = make_profile(p);
+  const int M = u->M, N = p->N;
+  for (int64_t k = 0; k < u->n_inst; ++k) {
+    const Scenario sc = make_scenario(prof, u, k);
+    Schedule s;
+    s.x.assign(M, std::vector<std::size_t>(N));
+    s.completion.assign(M, std::vector<double>(N + 1));
+    for (int m = 0; m < M; ++m) {
+      for (int n = 0; n < N; ++n) s.x[m][n] = (std::size_t)sc_in->x[((size_t)k * M + m) * N + n];
+      for (int n = 0; n <= N; ++n) s.completion[m][n] = sc_in->completion[((size_t)k * M + m) * (N + 1) + n];
+      s.freq.push_back(sc_in->freq[(size_t)k * M + m]);
+    }
+    for (int i = 0; i < sc_in->n_batches[k]; ++i) s.batch_start.push_back(sc_in->batch_start[(size_t)k * M * N + i]);
+    for (int c = 0; c < COINFER_N_CONSTRAINTS; ++c) counts[(size_t)k * COINFER_N_CONSTRAINTS + c] = 0;
+    double worst = 0.0;
+    try {
+      for (const Violation& v : validate(s, sc, tol)) {
+        for (int c = 0; c < COINFER_N_CONSTRAINTS; ++c)
+          if (v.constraint_id == ids[c]) ++counts[(size_t)k * COINFER_N_CONSTRAINTS + c];
+        worst = v.slack < worst ? v.slack : worst;
+      }
+      status[k] = COINFER_ST_OK;
+    } catch (const std::invalid_argument&) {
+      status[k] = COINFER_ST_BAD_BATCH_ID;
+    } catch (const std::out_of_range&) {
+      status[k] = COINFER_ST_BOUND_PAST_TABLE;
+    } catch (const std::domain_error&) {
+      status[k] = COINFER_ST_NONPOS_FREQ;
+    }
+    if (min_slack) min_slack[k] = status[k] == COINFER_ST_OK ? worst : 0.0;
   }
   return COINFER_OK;
 }

@@ -21,6 +21,10 @@ ST_OK, ST_INFEASIBLE = 0, 1
 ST_BAD_FREQ, ST_NEG_KAPPA, ST_BAD_RATE, ST_NEG_POWER = 10, 11, 12, 13
 ST_NEG_ARRIVAL, ST_EARLY_DEADLINE, ST_SHORT_TABLE = 14, 15, 16
 ST_ZERO_BOUND, ST_BOUND_PAST_TABLE = 17, 18
+ST_BAD_BATCH_ID, ST_NONPOS_FREQ = 19, 23
+N_CONSTRAINTS = 7
+CONSTRAINT_IDS = ["C7-batchsize", "C8-samesubtask", "C9-batchready", "C11-occupancy",
+                  "C12-precedence", "C15-deadline", "C17-initial"]
 MEM_HOST, MEM_DEVICE = 0, 1
 MAX_SUBTASKS = 16
 
@@ -125,6 +129,8 @@ PRODUCT_SYMBOLS = {
     "coinfer_baseline_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                          C.c_int32, C.POINTER(IpssaOut),
                                          C.POINTER(ScheduleOut)]),
+    "coinfer_validate_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                         C.POINTER(ScheduleOut), C.c_double, _i32p, _i32p, _dp]),
     "coinfer_best_partition": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
                                          _i32p, _dp, _dp, _u8p]),
     "coinfer_online_run": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),

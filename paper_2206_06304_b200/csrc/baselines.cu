@@ -675,6 +675,116 @@ __global__ void partition_kernel(AuxArgs a, const double* s, int32_t* split, dou
   }
 }
 
+// validate (schedule.hpp:139-209) as counts per constraint id, one thread
+// per instance; the same checks, in the same order (so the same first
+// exception), with the reference's arithmetic.
+__global__ void validate_kernel(AuxArgs a) {
+  const ProfileConst& P = a.P;
+  const int M = a.M, N = P.N;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.n_inst;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const Sched S = sched_of(a, k);
+    const size_t base = (size_t)k * M;
+    const int nb = *S.nb;
+    Scratch sc(a);
+    int* bsize = sc.take<int>((size_t)M * N);
+    int* bsub = sc.take<int>((size_t)M * N);
+    int* bmix = sc.take<int>((size_t)M * N);
+    int cnt[COINFER_N_CONSTRAINTS] = {0, 0, 0, 0, 0, 0, 0};
+    double worst = 0.0;
+    int st = COINFER_ST_OK;
+    auto hit = [&](int c, double slack) {
+      ++cnt[c];
+      worst = slack < worst ? slack : worst;
+    };
+    for (int q = 0; q < nb; ++q) bsize[q] = bsub[q] = bmix[q] = 0;
+    // batch_views (schedule.hpp:78-91): members in (m, n) order
+    for (int m = 0; m < M && st == COINFER_ST_OK; ++m)
+      for (int i = 0; i < N; ++i) {
+        const int id = S.x[(size_t)m * N + i];
+        if (id == 0) continue;
+        if (id > nb || id < 0) {
+          st = COINFER_ST_BAD_BATCH_ID;
+          break;
+        }
+        if (bsize[id - 1] == 0) bsub[id - 1] = i + 1;
+        else if (bsub[id - 1] != i + 1) bmix[id - 1] = 1;
+        ++bsize[id - 1];
+      }
+    const double tol = a.tol, ntol = -a.tol;
+    auto local_at = [&](int m, int n) { return n == 0 || S.x[(size_t)m * N + n - 1] == 0; };
+    auto comp = [&](int m, int n) { return S.comp[(size_t)m * (N + 1) + n]; };
+    if (st == COINFER_ST_OK) {
+      // C7 / C8
+      for (int q = 0; q < nb; ++q) {
+        if (bsize[q] == 0) hit(0, -1.0);
+        else if (bmix[q]) hit(1, -1.0);
+      }
+      // C17
+      for (int m = 0; m < M; ++m) {
+        const double d = __dsub_rn(comp(m, 0), a.arr[base + m]);
+        if (d < ntol || d > tol) hit(6, -(d < 0 ? -d : d));
+      }
+      // C9: every member's input at the edge by s_k
+      for (int m = 0; m < M; ++m)
+        for (int n = 1; n <= N; ++n) {
+          const int id = S.x[(size_t)m * N + n - 1];
+          if (id == 0) continue;
+          double ready = comp(m, n - 1);
+          if (local_at(m, n - 1)) ready = __dadd_rn(ready, __ddiv_rn(P.bits[n - 1], a.ru[base + m]));
+          const double slack = __dsub_rn(S.bstart[id - 1], ready);
+          if (slack < ntol) hit(2, slack);
+        }
+      // C11: consecutive batch ids
+      for (int q = 0; q + 1 < nb && st == COINFER_ST_OK; ++q) {
+        double busy = 0.0;
+        if (bsize[q] != 0) {
+          if (bsize[q] > P.bmax) {
+            st = COINFER_ST_BOUND_PAST_TABLE;
+            break;
+          }
+          busy = F(a, bsub[q], bsize[q]);
+        }
+        const double slack = __dsub_rn(__dsub_rn(S.bstart[q + 1], S.bstart[q]), busy);
+        if (slack < ntol) hit(3, slack);
+      }
+      // C12 / C15
+      for (int m = 0; m < M && st == COINFER_ST_OK; ++m) {
+        const double rd = a.rd ? a.rd[base + m] : a.ru[base + m];
+        for (int n = 1; n <= N; ++n) {
+          const int id = S.x[(size_t)m * N + n - 1];
+          double need;
+          if (id == 0) {
+            need = comp(m, n - 1);
+            if (n - 1 >= 1 && !local_at(m, n - 1)) need = __dadd_rn(need, __ddiv_rn(P.bits[n - 1], rd));
+            const double f = S.freq[m];
+            if (f <= 0.0) {  // local_latency throws (core_model.hpp:104-105)
+              st = COINFER_ST_NONPOS_FREQ;
+              break;
+            }
+            need = __dadd_rn(need, __ddiv_rn(P.work[n - 1], f));
+          } else {
+            if (bsize[id - 1] > P.bmax) {
+              st = COINFER_ST_BOUND_PAST_TABLE;
+              break;
+            }
+            need = __dadd_rn(S.bstart[id - 1], F(a, n, bsize[id - 1]));
+          }
+          const double slack = __dsub_rn(comp(m, n), need);
+          if (slack < ntol) hit(4, slack);
+        }
+        if (st != COINFER_ST_OK) break;
+        const double slack = __dsub_rn(a.dl[base + m], comp(m, N));
+        if (slack < ntol) hit(5, slack);
+      }
+    }
+    a.vstatus[k] = st;
+    for (int c = 0; c < COINFER_N_CONSTRAINTS; ++c)
+      a.vcounts[(size_t)k * COINFER_N_CONSTRAINTS + c] = st == COINFER_ST_OK ? cnt[c] : 0;
+    if (a.vslack) a.vslack[k] = st == COINFER_ST_OK ? worst : 0.0;
+  }
+}
+
 constexpr int kThreads = 128;
 
 }  // namespace
@@ -702,6 +812,11 @@ cudaError_t launch_materialize_og(const AuxArgs& a, cudaStream_t st) {
 
 cudaError_t launch_baseline(const AuxArgs& a, cudaStream_t st) {
   baseline_kernel<<<aux_grid(a.n_inst), kThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const AuxArgs& a, cudaStream_t st) {
+  validate_kernel<<<aux_grid(a.n_inst), kThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -862,6 +862,8 @@ const char* coinfer_status_message(int32_t status, const char* solver) {
     case COINFER_ST_NOT_RELEASED: return "online: users must be released at time zero";
     case COINFER_ST_FLOOR_ABOVE_LLOW: return "online: l_low below a user's all-local floor";
     case COINFER_ST_SLIPPED: return "online: task slipped below its local floor";
+    case COINFER_ST_BAD_BATCH_ID: return "schedule: batch id beyond start-time table";
+    case COINFER_ST_NONPOS_FREQ: return "local_latency: f must be positive";
   }
   return "unknown status";
 }
@@ -1074,6 +1076,96 @@ int coinfer_baseline_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
   if (sched && !sched_complete(sched))
     return fail(ctx, COINFER_E_ARG, "baseline: schedule arrays missing");
   return run_aux(ctx, profile, users, nullptr, Aux::Baseline, mode, out, nullptr, sched);
+}
+
+int coinfer_validate_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                           const coinfer_users* users, const coinfer_schedule_out* sched,
+                           double tol, int32_t* status, int32_t* counts, double* min_slack) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  int rc = check_users(ctx, users);
+  if (rc != COINFER_OK) return rc;
+  if (!sched_complete(sched)) return fail(ctx, COINFER_E_ARG, "validate: schedule arrays missing");
+  if (!status || !counts) return fail(ctx, COINFER_E_ARG, "validate: null output");
+  rc = check_profile(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+  if (users->n_inst == 0) return COINFER_OK;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  const size_t K = (size_t)users->n_inst, M = (size_t)users->M, N = (size_t)profile->N;
+  const bool host = users->mem == COINFER_MEM_HOST;
+  cfb::AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.P = make_const(profile);
+  a.n_inst = users->n_inst;
+  a.M = users->M;
+  a.arr = users->arrival;
+  a.dl = users->deadline;
+  a.ru = users->rate_up;
+  a.rd = users->rate_down;
+  a.sch = *sched;
+  a.tol = tol;
+  a.vstatus = status;
+  a.vcounts = counts;
+  a.vslack = min_slack;
+  Stager st{ctx};
+  if (host) {
+    plan_in(st, a.arr, K * M);
+    plan_in(st, a.dl, K * M);
+    plan_in(st, a.ru, K * M);
+    plan_in(st, a.rd, K * M);
+    plan_in_mut(st, a.sch.x, K * M * N);
+    plan_in_mut(st, a.sch.n_batches, K);
+    plan_in_mut(st, a.sch.batch_start, K * M * N);
+    plan_in_mut(st, a.sch.completion, K * M * (N + 1));
+    plan_in_mut(st, a.sch.freq, K * M);
+    plan_out(st, a.vstatus, K);
+    plan_out(st, a.vcounts, K * COINFER_N_CONSTRAINTS);
+    plan_out(st, a.vslack, K);
+  }
+  const size_t nlat = N * (size_t)profile->b_max;
+  const size_t lat_off = st.reserve(nlat * 8);
+  const int grid = cfb::aux_grid(users->n_inst);
+  a.scratch_per_thread = (cfb::aux_scratch_bytes((int)M, (int)N) + 255) & ~size_t(255);
+  const size_t scr_off = st.reserve((size_t)grid * 128 * a.scratch_per_thread);
+  rc = ensure_aux(ctx, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->aux;
+  cudaStream_t sp = ctx->stream;
+  if (host) {
+    patch(b, a.arr);
+    patch(b, a.dl);
+    patch(b, a.ru);
+    patch(b, a.rd);
+    patch(b, a.sch.x);
+    patch(b, a.sch.n_batches);
+    patch(b, a.sch.batch_start);
+    patch(b, a.sch.completion);
+    patch(b, a.sch.freq);
+    patch(b, a.vstatus);
+    patch(b, a.vcounts);
+    patch(b, a.vslack);
+    for (const auto& x : st.in) {
+      e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+    }
+  }
+  a.lat = reinterpret_cast<const double*>(b + lat_off);
+  e = cudaMemcpyAsync(b + lat_off, profile->latency, nlat * 8, cudaMemcpyHostToDevice, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D latency");
+  a.scratch = b + scr_off;
+  e = cfb::launch_validate(a, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+  if (host) {
+    for (const auto& x : st.back) {
+      e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+    }
+  }
+  e = cudaStreamSynchronize(sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "validate");
+  return COINFER_OK;
 }
 
 int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,

@@ -97,6 +97,11 @@ struct AuxArgs {
   int mode;                 // COINFER_BASELINE_*
   unsigned char* scratch;   // per-thread scratch, scratch_per_thread bytes each
   size_t scratch_per_thread;
+  // validate: tolerance and outputs
+  double tol;
+  int32_t* vstatus;         // [n_inst]
+  int32_t* vcounts;         // [n_inst * COINFER_N_CONSTRAINTS]
+  double* vslack;           // [n_inst] (optional)
 };
 
 size_t aux_scratch_bytes(int M, int N);
@@ -104,6 +109,7 @@ int aux_grid(int64_t n_inst);
 cudaError_t launch_materialize_ip(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_materialize_og(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_baseline(const AuxArgs& a, cudaStream_t st);
+cudaError_t launch_validate(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_partition(const AuxArgs& a, const double* s, int32_t* split, double* freq,
                              double* energy, uint8_t* feasible, cudaStream_t st);
 

@@ -292,6 +292,29 @@ class Engine:
             C.byref(pk.out_ip), C.byref(so) if so is not None else None))
         return Packed.arrays(pk.out_ip), (Packed.arrays(so) if so is not None else None)
 
+    def validate(self, profile, users: Dict, sched: Dict, tol: float = 1e-9):
+        """validate(schedule, scenario, tol) for every instance (schedule.hpp:139-209):
+        status [K], counts [K, 7] per constraint id (_abi.CONSTRAINT_IDS order)
+        and the most negative slack [K].  `sched` as returned by *_schedule()
+        or baseline()."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, False, False)
+        so = self._as_struct(_abi.ScheduleOut, _abi.SCHEDULE_FIELDS, sched)
+        K = pk.K
+        if mem == _abi.MEM_DEVICE:
+            dev = f"cuda:{self.device}"
+            st = torch.empty(K, dtype=torch.int32, device=dev)
+            cnt = torch.empty((K, _abi.N_CONSTRAINTS), dtype=torch.int32, device=dev)
+            sl = torch.empty(K, dtype=torch.float64, device=dev)
+        else:
+            st = np.zeros(K, np.int32)
+            cnt = np.zeros((K, _abi.N_CONSTRAINTS), np.int32)
+            sl = np.zeros(K)
+        self._check(self.lib.coinfer_validate_batch(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                    C.byref(so), float(tol), _ptr(st, C.c_int32),
+                                                    _ptr(cnt, C.c_int32), _ptr(sl, C.c_double)))
+        return dict(status=st, counts=cnt, min_slack=sl)
+
     def best_partition(self, profile, users: Dict, s=None):
         """best_partition (s: [n, N] start times) or local_only_choice (s None)
         for n single-user queries (users fields of shape (n, 1)); host memory."""

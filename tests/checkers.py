@@ -42,6 +42,7 @@ REF_SYMBOLS = {
     "ref_sweep_threads": (C.c_double, [_P, _U, C.POINTER(C.c_int64), C.c_int64, C.c_int, C.c_int,
                                        C.c_int, _dp, _dp]),
     "ref_schedule_batch": (C.c_int, [_P, _U, _dp, C.c_int, _i32p, C.POINTER(_abi.ScheduleOut)]),
+    "ref_validate_batch": (C.c_int, [_P, _U, C.POINTER(_abi.ScheduleOut), C.c_double, _i32p, _i32p, _dp]),
     "ref_baseline_batch": (C.c_int, [_P, _U, C.c_int, _IO, C.POINTER(_abi.ScheduleOut)]),
     "ref_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ref_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
@@ -151,6 +152,22 @@ def ref_baseline(profile, users, mode):
                                   _abi.BASELINE_MODES[mode], C.byref(pk.out_ip), C.byref(so))
     assert rc == 0, rc
     return Packed.arrays(pk.out_ip), Packed.arrays(so)
+
+
+def ref_validate(profile, users, sched, tol=1e-9):
+    """validate() through the reference: status, counts per constraint id, worst slack."""
+    pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+    arrays = {k: np.ascontiguousarray(_to_np(v)) for k, v in sched.items()}
+    ptrs = [arrays[n].ctypes.data_as(t) for n, t, _ in _abi.SCHEDULE_FIELDS]
+    so = _abi.ScheduleOut(*ptrs)
+    K = pk.K
+    st = np.zeros(K, np.int32)
+    cnt = np.zeros((K, _abi.N_CONSTRAINTS), np.int32)
+    sl = np.zeros(K)
+    assert ref().ref_validate_batch(C.byref(pk.profile), C.byref(pk.users), C.byref(so), float(tol),
+                                    st.ctypes.data_as(_i32p), cnt.ctypes.data_as(_i32p),
+                                    sl.ctypes.data_as(_dp)) == 0
+    return dict(status=st, counts=cnt, min_slack=sl)
 
 
 def assert_same_schedule(a: dict, b: dict, status, where=""):

@@ -177,7 +177,9 @@ TEST(Golden, OgThroughTheDropIn) {
       // a fallback plan carries lc_solve's user-order fold instead)
       double fold = 0.0;
       for (double x : p.group_energy) fold += x;
-      if (!p.fallback) EXPECT_TRUE(same_bits(fold, p.energy)) << where;
+      if (!p.fallback) {
+        EXPECT_TRUE(same_bits(fold, p.energy)) << where;
+      }
       Schedule norm = p.schedule;
       normalize(norm);
       EXPECT_EQ(norm.x, p.schedule.x) << where << " (device schedule is normalised)";
