@@ -66,14 +66,35 @@ def parse():
 
 # ----------------------------------------------------------------- inputs
 
-def make_inputs(args, rank, world):
-    """This rank's instances: weak scaling, `--n-inst` instances per rank, drawn
-    per 4096-instance block keyed by the global block index (shard.py)."""
-    from paper_2206_06304_b200 import profile_heavy
+def make_inputs(args, rank, world, eng=None):
+    """This rank's instances, weak scaling: `--n-inst` instances per rank,
+    global indices [lo, hi) (shard.py).  Instance k is the reference CLI's
+    k-th draw, sample_scenario with std::mt19937_64(sub_seed(seed, 1, k))
+    (coinfer_main.cpp:47-50, 346-350), generated on the GPU by
+    coinfer_sample_batch when `eng` is given (device tensors), else by the
+    numpy sampler of the same distribution (host; CPU-only runs)."""
+    from paper_2206_06304_b200 import profile_heavy, sub_seed
     from paper_2206_06304_b200.shard import make_instances, shard_range
     prof = profile_heavy(args.M)
     lo, hi = shard_range(args.n_inst, rank, world)
-    return prof, make_instances(prof, args.M, lo, hi, seed=args.seed), lo, hi
+    if eng is None:
+        return prof, make_instances(prof, args.M, lo, hi, seed=args.seed), lo, hi
+    seeds = sub_seed(args.seed, 1, np.arange(lo, hi, dtype=np.uint64))
+    users, st = eng.sample(prof, args.M, seeds, 0.25, 1.0, device=True)
+    assert int((st != 0).sum()) == 0
+    fields = ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline"]
+    return prof, {k: users[k] for k in fields}, lo, hi
+
+
+def reference_inputs(args, count):
+    """The first `count` instances of the same stream through the REFERENCE's
+    own generator (oracle/_ref: sample_scenario, mt19937_64, glibc libm)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import checkers as ck
+    from paper_2206_06304_b200 import sub_seed
+    seeds = sub_seed(args.seed, 1, np.arange(count, dtype=np.uint64))
+    prof, users = ck.ref_sample_scenarios(count, args.M, 0.25, 1.0, seeds, heavy=True)
+    return prof, users
 
 
 def feasibility_thresholds(prof):
@@ -209,7 +230,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        prof, users, lo, hi = make_inputs(args, 0, 1)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import checkers as ck
+        sample_n = min(args.n_inst, 8192)  # bounded: the CPU solves ~200 instances/s
+        if ck.ref() is not None:  # the reference CLI's own instances, by its own generator
+            prof, users = reference_inputs(args, sample_n)
+        else:
+            prof, users, _, _ = make_inputs(args, 0, 1)
+            users = {k: v[:sample_n] for k, v in users.items()}
         vals = []
         for s in range(args.warmup + args.steps):
             target = 2.0 if s < args.warmup else args.cpu_seconds
@@ -222,7 +250,8 @@ def main():
             "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the first instances of the reference CLI stream, by the reference generator",
             "config": {"workload": WORKLOAD, "n_inst_per_gpu": args.n_inst, "M": args.M},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
@@ -236,12 +265,13 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    prof, users, lo, hi = make_inputs(args, rank, world)
-    K = hi - lo
     eng = Engine(local)
     stream = torch.cuda.Stream(local)
-    dev = {k: torch.as_tensor(v).to(f"cuda:{local}") for k, v in users.items()}
+    with torch.cuda.stream(stream):
+        prof, dev, lo, hi = make_inputs(args, rank, world, eng)
     torch.cuda.synchronize()
+    K = hi - lo
+    users = {k: v.cpu().numpy() for k, v in dev.items()}  # host copy: e2e and cpu_baseline
 
     def barrier():
         if world > 1:
@@ -328,7 +358,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (sample_scenario distribution, numpy RNG, fixed seed)",
+            "data": ("synthetic: the reference CLI's instance stream, sample_scenario with "
+                     "mt19937_64(sub_seed(1,1,k)) for instance k, generated on the GPU "
+                     "(coinfer_sample_batch; rates within libm ulps of glibc)"),
             "config": {"workload": WORKLOAD, "n_inst_per_gpu": args.n_inst,
                        "n_inst_total": args.n_inst * world, "M": args.M, "N": prof.N,
                        "parallelism": f"instance shards x{world}",

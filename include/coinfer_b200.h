@@ -28,6 +28,7 @@
  *                                                                       schedule.hpp:93-113
  *   coinfer_baseline_batch <- baseline(const Scenario&, BaselineMode)   offline_solvers.hpp:390-612
  *   coinfer_validate_batch <- validate(const Schedule&, const Scenario&, double) schedule.hpp:139-209
+ *   coinfer_sample_batch  <- sample_scenario(cfg, profile, rng)        scenario_gen.hpp:113-173
  *   coinfer_best_partition <- best_partition / detail::local_only_choice offline_solvers.hpp:62-117
  *   coinfer_online_run    <- run_episode(OnlineEnv&, TimeWindowPolicy, horizon, seed)
  *                                                                       online_sim.hpp:131-249,312-371
@@ -315,6 +316,40 @@ int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,
 int coinfer_validate_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
                            const coinfer_users* users, const coinfer_schedule_out* sched,
                            double tol, int32_t* status, int32_t* counts, double* min_slack);
+
+/* Scenario generation on the device: sample_scenario(cfg, profile,
+   std::mt19937_64(seeds[k])) (scenario_gen.hpp:113-173) for every k.  The
+   RNG stream, positions, deadlines, f_max and kappa are the reference
+   generator's bit for bit; rates go through CUDA's log10/pow/log2 (within
+   1-2 ulp of glibc's).  The CLI seeds instance k of its sweep with
+   coinfer_sub_seed(root, 1, k) (coinfer_main.cpp:47-50,346-350). */
+typedef struct coinfer_sample_cfg {  /* ScenarioConfig (scenario_gen.hpp:49-84) */
+  double cell_radius, bandwidth, noise_dbm_hz, tx_power, uplink_power, downlink_power;
+  double edge_power, edge_efficiency, device_efficiency, alpha, shadow_sigma_db;
+  int32_t deadline_uniform; /* 0: DeadlineSpec::fixed(deadline_low); 1: uniform(low, high) */
+  int32_t reserved;
+  double deadline_low, deadline_high;
+} coinfer_sample_cfg;
+
+/* The same layout as coinfer_users, with writable arrays (an output). */
+typedef struct coinfer_users_mut {
+  int64_t n_inst;
+  int32_t M;
+  int32_t mem;
+  double *f_min, *f_max, *kappa, *rate_up, *power_up, *arrival, *deadline, *rate_down, *power_down;
+} coinfer_users_mut;
+
+#define COINFER_ST_NO_DEADLINE 24 /* runtime_error "sample_scenario: cannot draw a feasible deadline" */
+
+void coinfer_sample_cfg_defaults(coinfer_sample_cfg* cfg); /* ScenarioConfig{} with fixed(0.5) */
+uint64_t coinfer_sub_seed(uint64_t root, uint64_t component, uint64_t index);
+/* out->n_inst instances of out->M users; seeds[n_inst] in out->mem memory,
+   status[n_inst] (optional, same memory).  Config / profile errors return
+   COINFER_E_ARG with the reference's message (ScenarioConfig::check,
+   DnnProfile::check, sample_scenario's own tests). */
+int coinfer_sample_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                         const coinfer_sample_cfg* cfg, const uint64_t* seeds,
+                         coinfer_users_mut* out, int32_t* status);
 
 /* Run n_ep episodes; episode e simulates scenario e % users->n_inst (each a
    Scenario of users->M users; deadlines are only contract-checked) with

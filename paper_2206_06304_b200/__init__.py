@@ -11,4 +11,4 @@ Layers:
 """
 from ._abi import load_library  # noqa: F401
 from .engine import Engine, ProfileArrays, SolverError  # noqa: F401
-from .scenarios import profile_heavy, profile_light, sample_batch, synth_profile  # noqa: F401
+from .scenarios import profile_heavy, profile_light, sample_batch, sub_seed, synth_profile  # noqa: F401

@@ -83,6 +83,17 @@ BASELINE_LC, BASELINE_PS, BASELINE_FIFO, BASELINE_IPSSA_NP = 0, 1, 2, 3
 BASELINE_MODES = {"LC": BASELINE_LC, "PS": BASELINE_PS, "FIFO": BASELINE_FIFO,
                   "IPSSA_NP": BASELINE_IPSSA_NP}
 
+class SampleCfg(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("cell_radius", "bandwidth", "noise_dbm_hz", "tx_power",
+                                          "uplink_power", "downlink_power", "edge_power",
+                                          "edge_efficiency", "device_efficiency", "alpha",
+                                          "shadow_sigma_db")] + [
+        ("deadline_uniform", C.c_int32), ("reserved", C.c_int32),
+        ("deadline_low", C.c_double), ("deadline_high", C.c_double)]
+
+
+ST_NO_DEADLINE = 24
+
 ARRIVAL_BERNOULLI, ARRIVAL_IMMEDIATE = 0, 1
 SOLVER_IPSSA, SOLVER_OG = 0, 1
 POLICY_TW, POLICY_LOCAL = 0, 1
@@ -131,6 +142,10 @@ PRODUCT_SYMBOLS = {
                                          C.POINTER(ScheduleOut)]),
     "coinfer_validate_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                          C.POINTER(ScheduleOut), C.c_double, _i32p, _i32p, _dp]),
+    "coinfer_sample_cfg_defaults": (None, [C.POINTER(SampleCfg)]),
+    "coinfer_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
+    "coinfer_sample_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(SampleCfg),
+                                       C.POINTER(C.c_uint64), C.POINTER(Users), _i32p]),
     "coinfer_best_partition": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
                                          _i32p, _dp, _dp, _u8p]),
     "coinfer_online_run": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),

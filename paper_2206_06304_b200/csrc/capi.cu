@@ -864,6 +864,7 @@ const char* coinfer_status_message(int32_t status, const char* solver) {
     case COINFER_ST_SLIPPED: return "online: task slipped below its local floor";
     case COINFER_ST_BAD_BATCH_ID: return "schedule: batch id beyond start-time table";
     case COINFER_ST_NONPOS_FREQ: return "local_latency: f must be positive";
+    case COINFER_ST_NO_DEADLINE: return "sample_scenario: cannot draw a feasible deadline";
   }
   return "unknown status";
 }
@@ -1165,6 +1166,125 @@ int coinfer_validate_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
   }
   e = cudaStreamSynchronize(sp);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "validate");
+  return COINFER_OK;
+}
+
+void coinfer_sample_cfg_defaults(coinfer_sample_cfg* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->cell_radius = 100.0;
+  c->bandwidth = 1e6;
+  c->noise_dbm_hz = -174.0;
+  c->tx_power = 0.05;
+  c->uplink_power = 1.0;
+  c->downlink_power = 1.0;
+  c->edge_power = 300.0;
+  c->edge_efficiency = 48.75;
+  c->device_efficiency = 48.75;
+  c->alpha = 1.0;
+  c->shadow_sigma_db = 8.0;
+  c->deadline_uniform = 0;
+  c->deadline_low = 0.5;
+  c->deadline_high = 0.5;
+}
+
+uint64_t coinfer_sub_seed(uint64_t root, uint64_t component, uint64_t index) {
+  auto mix64 = [](uint64_t x) {  // splitmix64 finalizer (ddpg.hpp:272-277)
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d4a9749d57afbbull;
+    return x ^ (x >> 31);
+  };
+  return mix64(mix64(root ^ (component * 0x9e3779b97f4a7c15ull)) + index);
+}
+
+int coinfer_sample_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                         const coinfer_sample_cfg* cfg, const uint64_t* seeds,
+                         coinfer_users_mut* out, int32_t* status) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  if (!cfg || !out) return fail(ctx, COINFER_E_ARG, "sample: null argument");
+  const coinfer_sample_cfg& c = *cfg;
+  // ScenarioConfig::check (scenario_gen.hpp:68-82)
+  if (out->M <= 0) return fail(ctx, COINFER_E_ARG, "config: users must be positive");
+  if (c.cell_radius <= 0.0 || c.bandwidth <= 0.0 || c.tx_power <= 0.0 || c.uplink_power < 0.0 ||
+      c.downlink_power < 0.0 || c.edge_power <= 0.0 || c.edge_efficiency <= 0.0 ||
+      c.device_efficiency <= 0.0 || c.alpha <= 0.0 || c.shadow_sigma_db < 0.0)
+    return fail(ctx, COINFER_E_ARG, "config: physical quantities must be positive");
+  if (!c.deadline_uniform) {
+    if (c.deadline_low <= 0.0) return fail(ctx, COINFER_E_ARG, "config: deadline must be positive");
+  } else if (c.deadline_low <= 0.0 || c.deadline_high < c.deadline_low) {
+    return fail(ctx, COINFER_E_ARG, "config: bad deadline range");
+  }
+  int rc = check_profile(ctx, profile);
+  if (rc != COINFER_OK) return fail(ctx, COINFER_E_ARG, ctx->err);
+  if (profile->b_max < out->M)
+    return fail(ctx, COINFER_E_ARG, "sample_scenario: latency table shorter than user count");
+  const cfb::ProfileConst P = make_const(profile);
+  const double total_work = P.prefix[P.N];
+  const double fmax = 1.0 / c.alpha, floor_ = total_work / fmax;
+  if (!c.deadline_uniform && c.deadline_low < floor_)
+    return fail(ctx, COINFER_E_ARG, "sample_scenario: deadline below the all-local floor");
+  if (c.deadline_uniform && c.deadline_high < floor_)
+    return fail(ctx, COINFER_E_ARG, "sample_scenario: deadline range below the all-local floor");
+  if (out->n_inst < 0) return fail(ctx, COINFER_E_ARG, "sample: negative size");
+  if (out->n_inst == 0) return COINFER_OK;
+  if (!seeds || !out->f_min || !out->f_max || !out->kappa || !out->rate_up || !out->power_up ||
+      !out->arrival || !out->deadline)
+    return fail(ctx, COINFER_E_ARG, "sample: null array");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  const size_t K = (size_t)out->n_inst, M = (size_t)out->M;
+  cudaStream_t sp = ctx->stream;
+  if (out->mem == COINFER_MEM_DEVICE) {
+    e = cfb::launch_sample(c, total_work, out->M, out->n_inst,
+                           reinterpret_cast<const unsigned long long*>(seeds), *out, status, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    ctx->launches += 1;
+    return COINFER_OK;
+  }
+  Stager st{ctx};
+  coinfer_users_mut d = *out;
+  const uint64_t* sd = seeds;
+  plan_in(st, sd, K);
+  plan_out(st, d.f_min, K * M);
+  plan_out(st, d.f_max, K * M);
+  plan_out(st, d.kappa, K * M);
+  plan_out(st, d.rate_up, K * M);
+  plan_out(st, d.power_up, K * M);
+  plan_out(st, d.arrival, K * M);
+  plan_out(st, d.deadline, K * M);
+  plan_out(st, d.rate_down, K * M);
+  plan_out(st, d.power_down, K * M);
+  plan_out(st, status, K);
+  rc = ensure_aux(ctx, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->aux;
+  patch(b, sd);
+  patch(b, d.f_min);
+  patch(b, d.f_max);
+  patch(b, d.kappa);
+  patch(b, d.rate_up);
+  patch(b, d.power_up);
+  patch(b, d.arrival);
+  patch(b, d.deadline);
+  patch(b, d.rate_down);
+  patch(b, d.power_down);
+  patch(b, status);
+  for (const auto& x : st.in) {
+    e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D seeds");
+  }
+  e = cfb::launch_sample(c, total_work, out->M, out->n_inst, reinterpret_cast<const unsigned long long*>(sd),
+                         d, status, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+  for (const auto& x : st.back) {
+    e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H users");
+  }
+  e = cudaStreamSynchronize(sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "sample");
   return COINFER_OK;
 }
 

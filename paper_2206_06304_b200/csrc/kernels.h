@@ -110,6 +110,9 @@ cudaError_t launch_materialize_ip(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_materialize_og(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_baseline(const AuxArgs& a, cudaStream_t st);
 cudaError_t launch_validate(const AuxArgs& a, cudaStream_t st);
+cudaError_t launch_sample(const coinfer_sample_cfg& cfg, double total_work, int M, int64_t n_inst,
+                          const unsigned long long* seeds, const coinfer_users_mut& out, int32_t* status,
+                          cudaStream_t st);
 cudaError_t launch_partition(const AuxArgs& a, const double* s, int32_t* split, double* freq,
                              double* energy, uint8_t* feasible, cudaStream_t st);
 

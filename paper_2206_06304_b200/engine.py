@@ -315,6 +315,46 @@ class Engine:
                                                     _ptr(cnt, C.c_int32), _ptr(sl, C.c_double)))
         return dict(status=st, counts=cnt, min_slack=sl)
 
+    def sample(self, profile, M: int, seeds, low: float = 0.25, high: float = 1.0,
+               device: bool = False, **cfg):
+        """sample_scenario (scenario_gen.hpp:113-173) on the GPU, one instance
+        per seed (std::mt19937_64(seed)); `cfg` overrides ScenarioConfig
+        fields (bandwidth, alpha, shadow_sigma_db, ...).  low == high: fixed
+        deadlines.  Returns the SoA user dict (numpy, or CUDA tensors with
+        device=True) and per-instance status."""
+        c = _abi.SampleCfg()
+        self.lib.coinfer_sample_cfg_defaults(C.byref(c))
+        for k, v in cfg.items():
+            setattr(c, k, float(v))
+        c.deadline_uniform = 0 if low == high else 1
+        c.deadline_low, c.deadline_high = float(low), float(high)
+        p = as_profile(profile)
+        pk_prof = _abi.Profile(p.N, p.b_max, _ptr(p.work, C.c_double), _ptr(p.data_bits, C.c_double),
+                               _ptr(p.latency, C.c_double))
+        K = len(seeds)
+        if device:
+            dev = f"cuda:{self.device}"
+            s = self.lib.coinfer_ctx_set_stream(self.ctx, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+            sd = torch.as_tensor(np.asarray(seeds, dtype=np.uint64).view(np.int64), device=dev)
+            out = {f: torch.empty((K, M), dtype=torch.float64, device=dev) for f in _abi.USER_FIELDS}
+            st = torch.empty(K, dtype=torch.int32, device=dev)
+            mem = _abi.MEM_DEVICE
+        else:
+            self.lib.coinfer_ctx_reset_stream(self.ctx)
+            sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+            out = {f: np.zeros((K, M)) for f in _abi.USER_FIELDS}
+            st = np.zeros(K, np.int32)
+            mem = _abi.MEM_HOST
+        u = _abi.Users(K, M, mem, *[_ptr(out[f], C.c_double) for f in _abi.USER_FIELDS])
+        self._check(self.lib.coinfer_sample_batch(self.ctx, C.byref(pk_prof), C.byref(c),
+                                                  _ptr(sd, C.c_uint64), C.byref(u), _ptr(st, C.c_int32)))
+        return out, st
+
+    def sub_seed(self, root: int, component: int, index) -> np.ndarray:
+        """The CLI's per-instance seeds sub_seed(root, component, k) (coinfer_main.cpp:47-50)."""
+        idx = np.atleast_1d(np.asarray(index, dtype=np.uint64))
+        return np.array([self.lib.coinfer_sub_seed(root, component, int(i)) for i in idx], dtype=np.uint64)
+
     def best_partition(self, profile, users: Dict, s=None):
         """best_partition (s: [n, N] start times) or local_only_choice (s None)
         for n single-user queries (users fields of shape (n, 1)); host memory."""

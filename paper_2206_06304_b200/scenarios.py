@@ -77,3 +77,21 @@ def sample_batch(n_inst: int, M: int, profile: ProfileArrays, low: float = 0.25,
     return dict(f_min=np.zeros(shape), f_max=one * f_max, kappa=one * kappa, rate_up=rate,
                 power_up=one * uplink_power, arrival=np.zeros(shape), deadline=dl,
                 rate_down=rate.copy(), power_down=one * uplink_power)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finalizer (ddpg.hpp:272-277), vectorised over uint64."""
+    x = (x + np.uint64(0x9e3779b97f4a7c15)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)).astype(np.uint64)
+    x = ((x ^ (x >> np.uint64(27))) * np.uint64(0x94d4a9749d57afbb)).astype(np.uint64)
+    return x ^ (x >> np.uint64(31))
+
+
+def sub_seed(root: int, component: int, index) -> np.ndarray:
+    """The CLI's per-stream seeds (coinfer_main.cpp:47-50):
+    mix64(mix64(root ^ component * golden) + index), vectorised over index."""
+    with np.errstate(over="ignore"):
+        r = np.uint64(root) ^ (np.uint64(component) * np.uint64(0x9e3779b97f4a7c15))
+        base = _mix64(np.array([r], dtype=np.uint64))[0]
+        idx = np.asarray(index, dtype=np.uint64)
+        return _mix64((base + idx).astype(np.uint64))
