@@ -29,6 +29,7 @@
  *   coinfer_baseline_batch <- baseline(const Scenario&, BaselineMode)   offline_solvers.hpp:390-612
  *   coinfer_validate_batch <- validate(const Schedule&, const Scenario&, double) schedule.hpp:139-209
  *   coinfer_sample_batch  <- sample_scenario(cfg, profile, rng)        scenario_gen.hpp:113-173
+ *   coinfer_oracle_*_batch <- oracle_structured / oracle_grouping(_contiguous) oracles.hpp:28-225
  *   coinfer_best_partition <- best_partition / detail::local_only_choice offline_solvers.hpp:62-117
  *   coinfer_online_run    <- run_episode(OnlineEnv&, TimeWindowPolicy, horizon, seed)
  *                                                                       online_sim.hpp:131-249,312-371
@@ -340,6 +341,7 @@ typedef struct coinfer_users_mut {
 } coinfer_users_mut;
 
 #define COINFER_ST_NO_DEADLINE 24 /* runtime_error "sample_scenario: cannot draw a feasible deadline" */
+#define COINFER_ST_TOO_LARGE 25   /* invalid_argument "...: instance too large to enumerate" (oracles) */
 
 void coinfer_sample_cfg_defaults(coinfer_sample_cfg* cfg); /* ScenarioConfig{} with fixed(0.5) */
 uint64_t coinfer_sub_seed(uint64_t root, uint64_t component, uint64_t index);
@@ -350,6 +352,24 @@ uint64_t coinfer_sub_seed(uint64_t root, uint64_t component, uint64_t index);
 int coinfer_sample_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
                          const coinfer_sample_cfg* cfg, const uint64_t* seeds,
                          coinfer_users_mut* out, int32_t* status);
+
+/* The reference's brute-force oracles (oracles.hpp), one CTA per instance:
+     oracle_structured(sc, deadline[k], b[k])      :28-93  ((N+1)^M <= 2e6)
+     oracle_grouping_contiguous(sc) / oracle_grouping(sc)   :131-225
+                                                   (M <= 16 / M <= 9)
+   Outputs mirror StructuredOracle / GroupingOracle: energy (+inf when
+   infeasible), split or group_of_user (index of the user's group in rising
+   deadline order), fallback, n_groups, feasible; status COINFER_ST_TOO_LARGE
+   when the reference would refuse to enumerate.  No contract checks (the
+   oracles do none).  Every output array is required. */
+int coinfer_oracle_structured_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                                    const coinfer_users* users, const double* deadline,
+                                    const int32_t* b, int32_t* status, double* energy,
+                                    uint8_t* split, uint8_t* fallback, uint8_t* feasible);
+int coinfer_oracle_grouping_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                                  const coinfer_users* users, int32_t contiguous, int32_t* status,
+                                  double* energy, int32_t* n_groups, int32_t* group_of_user,
+                                  uint8_t* feasible);
 
 /* Run n_ep episodes; episode e simulates scenario e % users->n_inst (each a
    Scenario of users->M users; deadlines are only contract-checked) with

@@ -334,6 +334,30 @@ double ref_oracle_grouping_contiguous(const coinfer_profile* p, const coinfer_us
   return o.energy;
 }
 
+// oracle_structured with outputs; the group ids of the grouping oracles
+// (index of the user's group in the oracle's rising-deadline order).
+double ref_oracle_structured(const coinfer_profile* p, const coinfer_users* u, int64_t k,
+                             double deadline, int32_t b, uint8_t* split, uint8_t* fallback,
+                             uint8_t* feasible) {
+  const Scenario sc = make_scenario(make_profile(p), u, k);
+  const StructuredOracle o = oracle_structured(sc, deadline, (std::size_t)b);
+  *fallback = o.fallback;
+  *feasible = o.feasible;
+  for (int m = 0; m < u->M; ++m) split[m] = o.feasible ? (uint8_t)o.split[m] : 0;
+  return o.energy;
+}
+
+double ref_oracle_groups(const coinfer_profile* p, const coinfer_users* u, int64_t k, int contiguous,
+                         int32_t* n_groups, int32_t* group_of_user) {
+  const Scenario sc = make_scenario(make_profile(p), u, k);
+  const GroupingOracle o = contiguous ? oracle_grouping_contiguous(sc) : oracle_grouping(sc);
+  *n_groups = o.feasible ? (int32_t)o.groups.size() : 0;
+  if (o.feasible)
+    for (std::size_t g = 0; g < o.groups.size(); ++g)
+      for (std::size_t m : o.groups[g]) group_of_user[m] = (int32_t)g;
+  return o.energy;
+}
+
 double ref_oracle_grouping(const coinfer_profile* p, const coinfer_users* u, int64_t k,
                            int32_t* n_groups) {
   const Scenario sc = make_scenario(make_profile(p), u, k);

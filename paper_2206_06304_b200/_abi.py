@@ -93,6 +93,7 @@ class SampleCfg(C.Structure):
 
 
 ST_NO_DEADLINE = 24
+ST_TOO_LARGE = 25
 
 ARRIVAL_BERNOULLI, ARRIVAL_IMMEDIATE = 0, 1
 SOLVER_IPSSA, SOLVER_OG = 0, 1
@@ -146,6 +147,10 @@ PRODUCT_SYMBOLS = {
     "coinfer_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
     "coinfer_sample_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(SampleCfg),
                                        C.POINTER(C.c_uint64), C.POINTER(Users), _i32p]),
+    "coinfer_oracle_structured_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                                  _dp, _i32p, _i32p, _dp, _u8p, _u8p, _u8p]),
+    "coinfer_oracle_grouping_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                                C.c_int32, _i32p, _dp, _i32p, _i32p, _u8p]),
     "coinfer_best_partition": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
                                          _i32p, _dp, _dp, _u8p]),
     "coinfer_online_run": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),

@@ -865,6 +865,10 @@ const char* coinfer_status_message(int32_t status, const char* solver) {
     case COINFER_ST_BAD_BATCH_ID: return "schedule: batch id beyond start-time table";
     case COINFER_ST_NONPOS_FREQ: return "local_latency: f must be positive";
     case COINFER_ST_NO_DEADLINE: return "sample_scenario: cannot draw a feasible deadline";
+    case COINFER_ST_TOO_LARGE:
+      if (s == "structured") return "oracle_structured: instance too large to enumerate";
+      if (s == "contiguous") return "oracle_grouping_contiguous: instance too large to enumerate";
+      return "oracle_grouping: instance too large to enumerate";
   }
   return "unknown status";
 }
@@ -1286,6 +1290,128 @@ int coinfer_sample_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
   e = cudaStreamSynchronize(sp);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "sample");
   return COINFER_OK;
+}
+
+namespace {
+// Shared driver of the two oracle entry points (host batches staged whole).
+int run_oracle(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+               cfb::OracleArgs a, bool structured) {
+  if (!ctx) return COINFER_E_ARG;
+  ctx->err.clear();
+  int rc = check_users(ctx, users);
+  if (rc != COINFER_OK) return rc;
+  rc = check_profile(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+  if (users->n_inst == 0) return COINFER_OK;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  rc = upload_latency(ctx, profile);
+  if (rc != COINFER_OK) return rc;
+  const size_t K = (size_t)users->n_inst, M = (size_t)users->M;
+  a.P = make_const(profile);
+  a.lat = ctx->d_lat;
+  a.n_inst = users->n_inst;
+  a.M = users->M;
+  a.fmin = users->f_min;
+  a.fmax = users->f_max;
+  a.kappa = users->kappa;
+  a.ru = users->rate_up;
+  a.pu = users->power_up;
+  a.arr = users->arrival;
+  a.dl = users->deadline;
+  cudaStream_t sp = ctx->stream;
+  if (users->mem == COINFER_MEM_DEVICE) {
+    e = structured ? cfb::launch_oracle_structured(a, sp) : cfb::launch_oracle_grouping(a, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    ctx->launches += 1;
+    return COINFER_OK;
+  }
+  Stager st{ctx};
+  plan_in(st, a.fmin, K * M);
+  plan_in(st, a.fmax, K * M);
+  plan_in(st, a.kappa, K * M);
+  plan_in(st, a.ru, K * M);
+  plan_in(st, a.pu, K * M);
+  plan_in(st, a.arr, K * M);
+  plan_in(st, a.dl, K * M);
+  plan_in(st, a.deadline, K);
+  plan_in(st, a.b, K);
+  plan_out(st, a.status, K);
+  plan_out(st, a.energy, K);
+  plan_out(st, a.split, K * M);
+  plan_out(st, a.fallback, K);
+  plan_out(st, a.feasible, K);
+  plan_out(st, a.n_groups, K);
+  plan_out(st, a.group_of_user, K * M);
+  rc = ensure_aux(ctx, st.used);
+  if (rc != COINFER_OK) return rc;
+  unsigned char* b = ctx->aux;
+  patch(b, a.fmin);
+  patch(b, a.fmax);
+  patch(b, a.kappa);
+  patch(b, a.ru);
+  patch(b, a.pu);
+  patch(b, a.arr);
+  patch(b, a.dl);
+  patch(b, a.deadline);
+  patch(b, a.b);
+  patch(b, a.status);
+  patch(b, a.energy);
+  patch(b, a.split);
+  patch(b, a.fallback);
+  patch(b, a.feasible);
+  patch(b, a.n_groups);
+  patch(b, a.group_of_user);
+  for (const auto& x : st.in) {
+    e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D inputs");
+  }
+  e = structured ? cfb::launch_oracle_structured(a, sp) : cfb::launch_oracle_grouping(a, sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+  ctx->launches += 1;
+  for (const auto& x : st.back) {
+    e = cudaMemcpyAsync(x.host, b + x.off, x.bytes, cudaMemcpyDeviceToHost, sp);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H outputs");
+  }
+  e = cudaStreamSynchronize(sp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "oracle");
+  return COINFER_OK;
+}
+}  // namespace
+
+int coinfer_oracle_structured_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                                    const coinfer_users* users, const double* deadline,
+                                    const int32_t* b, int32_t* status, double* energy,
+                                    uint8_t* split, uint8_t* fallback, uint8_t* feasible) {
+  if (!deadline || !b || !status || !energy || !split || !fallback || !feasible)
+    return fail(ctx, COINFER_E_ARG, "oracle_structured: null argument");
+  cfb::OracleArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.deadline = deadline;
+  a.b = b;
+  a.status = status;
+  a.energy = energy;
+  a.split = split;
+  a.fallback = fallback;
+  a.feasible = feasible;
+  return run_oracle(ctx, profile, users, a, true);
+}
+
+int coinfer_oracle_grouping_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
+                                  const coinfer_users* users, int32_t contiguous, int32_t* status,
+                                  double* energy, int32_t* n_groups, int32_t* group_of_user,
+                                  uint8_t* feasible) {
+  if (!status || !energy || !n_groups || !group_of_user || !feasible)
+    return fail(ctx, COINFER_E_ARG, "oracle_grouping: null argument");
+  cfb::OracleArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.contiguous = contiguous ? 1 : 0;
+  a.status = status;
+  a.energy = energy;
+  a.n_groups = n_groups;
+  a.group_of_user = group_of_user;
+  a.feasible = feasible;
+  return run_oracle(ctx, profile, users, a, false);
 }
 
 int coinfer_best_partition(coinfer_ctx* ctx, const coinfer_profile* profile,

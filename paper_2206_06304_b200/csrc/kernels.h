@@ -104,6 +104,28 @@ struct AuxArgs {
   double* vslack;           // [n_inst] (optional)
 };
 
+// Arguments of the brute-force oracle kernels (oracles.cu), device memory.
+struct OracleArgs {
+  ProfileConst P;
+  const double* lat;
+  int64_t n_inst;
+  int M;
+  const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl;
+  const double* deadline;  // structured: common deadline per instance
+  const int32_t* b;        // structured: bound per instance
+  int contiguous;          // grouping: 1 = cut patterns only
+  int32_t* status;
+  double* energy;
+  uint8_t* split;          // structured [K*M]
+  uint8_t* fallback;       // structured [K]
+  uint8_t* feasible;       // [K]
+  int32_t* n_groups;       // grouping [K]
+  int32_t* group_of_user;  // grouping [K*M]
+};
+
+cudaError_t launch_oracle_structured(const OracleArgs& a, cudaStream_t st);
+cudaError_t launch_oracle_grouping(const OracleArgs& a, cudaStream_t st);
+
 size_t aux_scratch_bytes(int M, int N);
 int aux_grid(int64_t n_inst);
 cudaError_t launch_materialize_ip(const AuxArgs& a, cudaStream_t st);

@@ -315,6 +315,37 @@ class Engine:
                                                     _ptr(cnt, C.c_int32), _ptr(sl, C.c_double)))
         return dict(status=st, counts=cnt, min_slack=sl)
 
+    def oracle_structured(self, profile, users: Dict, deadline, b):
+        """oracle_structured(sc, deadline[k], b[k]) (oracles.hpp:28-93) on the GPU:
+        exhaustive over the (N+1)^M split vectors; host memory."""
+        pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+        K, M = pk.K, pk.M
+        d = np.ascontiguousarray(deadline, dtype=np.float64)
+        bb = np.ascontiguousarray(b, dtype=np.int32)
+        out = dict(status=np.zeros(K, np.int32), energy=np.zeros(K), split=np.zeros((K, M), np.uint8),
+                   fallback=np.zeros(K, np.uint8), feasible=np.zeros(K, np.uint8))
+        self.lib.coinfer_ctx_reset_stream(self.ctx)
+        self._check(self.lib.coinfer_oracle_structured_batch(
+            self.ctx, C.byref(pk.profile), C.byref(pk.users), _ptr(d, C.c_double), _ptr(bb, C.c_int32),
+            _ptr(out["status"], C.c_int32), _ptr(out["energy"], C.c_double), _ptr(out["split"], C.c_uint8),
+            _ptr(out["fallback"], C.c_uint8), _ptr(out["feasible"], C.c_uint8)))
+        return out
+
+    def oracle_grouping(self, profile, users: Dict, contiguous: bool = True):
+        """oracle_grouping_contiguous / oracle_grouping (oracles.hpp:131-225) on the
+        GPU: every cut pattern (M <= 16) or every set partition (M <= 9); host memory."""
+        pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+        K, M = pk.K, pk.M
+        out = dict(status=np.zeros(K, np.int32), energy=np.zeros(K), n_groups=np.zeros(K, np.int32),
+                   group_of_user=np.zeros((K, M), np.int32), feasible=np.zeros(K, np.uint8))
+        self.lib.coinfer_ctx_reset_stream(self.ctx)
+        self._check(self.lib.coinfer_oracle_grouping_batch(
+            self.ctx, C.byref(pk.profile), C.byref(pk.users), 1 if contiguous else 0,
+            _ptr(out["status"], C.c_int32), _ptr(out["energy"], C.c_double),
+            _ptr(out["n_groups"], C.c_int32), _ptr(out["group_of_user"], C.c_int32),
+            _ptr(out["feasible"], C.c_uint8)))
+        return out
+
     def sample(self, profile, M: int, seeds, low: float = 0.25, high: float = 1.0,
                device: bool = False, **cfg):
         """sample_scenario (scenario_gen.hpp:113-173) on the GPU, one instance

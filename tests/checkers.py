@@ -44,6 +44,10 @@ REF_SYMBOLS = {
     "ref_schedule_batch": (C.c_int, [_P, _U, _dp, C.c_int, _i32p, C.POINTER(_abi.ScheduleOut)]),
     "ref_validate_batch": (C.c_int, [_P, _U, C.POINTER(_abi.ScheduleOut), C.c_double, _i32p, _i32p, _dp]),
     "ref_baseline_batch": (C.c_int, [_P, _U, C.c_int, _IO, C.POINTER(_abi.ScheduleOut)]),
+    "ref_oracle_structured": (C.c_double, [_P, _U, C.c_int64, C.c_double, C.c_int32,
+                                           C.POINTER(C.c_uint8), C.POINTER(C.c_uint8),
+                                           C.POINTER(C.c_uint8)]),
+    "ref_oracle_groups": (C.c_double, [_P, _U, C.c_int64, C.c_int, _i32p, _i32p]),
     "ref_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ref_sub_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
     "ref_rng_new": (C.c_void_p, [C.c_uint64]),
@@ -168,6 +172,38 @@ def ref_validate(profile, users, sched, tol=1e-9):
                                     st.ctypes.data_as(_i32p), cnt.ctypes.data_as(_i32p),
                                     sl.ctypes.data_as(_dp)) == 0
     return dict(status=st, counts=cnt, min_slack=sl)
+
+
+def ref_oracle_structured(profile, users, deadline, b):
+    """oracle_structured per instance through the reference."""
+    pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+    K, M = pk.K, pk.M
+    out = dict(energy=np.zeros(K), split=np.zeros((K, M), np.uint8), fallback=np.zeros(K, np.uint8),
+               feasible=np.zeros(K, np.uint8))
+    for k in range(K):
+        sp = np.zeros(M, np.uint8)
+        fb, fe = C.c_uint8(), C.c_uint8()
+        out["energy"][k] = ref().ref_oracle_structured(C.byref(pk.profile), C.byref(pk.users), k,
+                                                       float(deadline[k]), int(b[k]),
+                                                       sp.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                                       C.byref(fb), C.byref(fe))
+        out["split"][k], out["fallback"][k], out["feasible"][k] = sp, fb.value, fe.value
+    return out
+
+
+def ref_oracle_groups(profile, users, contiguous):
+    """oracle_grouping(_contiguous) per instance through the reference."""
+    pk = Packed(profile, users, _abi.MEM_HOST, False, False)
+    K, M = pk.K, pk.M
+    out = dict(energy=np.zeros(K), n_groups=np.zeros(K, np.int32), group_of_user=np.zeros((K, M), np.int32))
+    for k in range(K):
+        ng = C.c_int32()
+        gu = np.zeros(M, np.int32)
+        out["energy"][k] = ref().ref_oracle_groups(C.byref(pk.profile), C.byref(pk.users), k,
+                                                   1 if contiguous else 0, C.byref(ng),
+                                                   gu.ctypes.data_as(_i32p))
+        out["n_groups"][k], out["group_of_user"][k] = ng.value, gu
+    return out
 
 
 def assert_same_schedule(a: dict, b: dict, status, where=""):
