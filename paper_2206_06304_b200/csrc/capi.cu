@@ -271,6 +271,9 @@ int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st)
   L.St = reinterpret_cast<double*>(take(8 * T));
   L.bstar = reinterpret_cast<uint16_t*>(take(2 * T));
   L.par = reinterpret_cast<uint16_t*>(take(2 * T));
+  L.pfit = reinterpret_cast<uint16_t*>(take(2 * T));
+  L.argpm = reinterpret_cast<uint16_t*>(take(2 * T));
+  L.slast = reinterpret_cast<double*>(take(8 * (size_t)M));
   L.rec = reinterpret_cast<double*>(take((size_t)M * cfb::rec_size(N) * 8));
   L.dls = reinterpret_cast<double*>(take(8 * (size_t)M));
   L.sumlat = reinterpret_cast<double*>(take(8 * ((size_t)M + 2)));
@@ -310,7 +313,7 @@ int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st)
     }
     cudaError_t e = cfb::launch_large(L, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "large-instance launch");
-    ctx->launches += 5;
+    ctx->launches += 6;
   }
   return COINFER_OK;
 }

@@ -74,9 +74,9 @@ struct LargeArgs {
   // workspace
   int* status;  // INT_MAX, or the first failing user * 32 + code
   int* simple;  // all arrivals and f_min zero
-  double *rec, *dls, *sumlat, *G, *St, *ipres, *fpos, *genergy;
+  double *rec, *dls, *sumlat, *G, *St, *ipres, *fpos, *genergy, *slast;
   int *order, *rank, *b0, *spos, *gid;
-  uint16_t *bstar, *par, *ipb;
+  uint16_t *bstar, *par, *ipb, *pfit, *argpm;
   coinfer_ipssa_out ip;
   coinfer_og_out og;
 };

@@ -12,13 +12,16 @@
 //                 passes of 32 lanes, each pass one left fold over j; the
 //                 warp-wide lexicographic argmin (energy asc, b desc) per cell
 //                 merges into the row with `<=` (later passes carry larger b)
+//   large_pfit    one thread per DP cell: the feasible-prev prefix length
+//                 (groups_fit is monotone in prev), before the DP
 //   large_finish  one CTA: the grouping DP over M sequential stages
-//                 (offline_solvers.hpp:313-330) with the column S[.][i-1] kept
-//                 as a prefix minimum in shared memory, so each cell is two
-//                 binary searches (value, then the reference's smallest prev);
-//                 best_i, backtrack, stitch, lc fallback, IP-SSA outputs.
-// G is an upper triangle in global memory; S is stored transposed (lower
-// triangle, St[j][p] = S[p][j]) so a stage reads its column contiguously.
+//                 (offline_solvers.hpp:313-330), the same O(1)-per-cell scheme
+//                 as solve_core.cuh: the triangle holds column prefix minima
+//                 and their first positions (running values of each column in
+//                 shared memory), so a cell is one gather plus a rare binary
+//                 search; best_i, backtrack, stitch, lc fallback, IP-SSA outputs.
+// G, the prefix minima (St) and the u16 triangles are upper triangles in
+// global memory, row-major.
 
 #include "solve_core.cuh"
 
@@ -29,7 +32,7 @@ namespace {
 __device__ __forceinline__ long long tri_u(long long i, long long j, long long M) {
   return i * M - ((i * (i - 1)) >> 1) + (j - i);  // upper triangle, row-major
 }
-__device__ __forceinline__ long long tri_l(long long j, long long p) {
+[[maybe_unused]] __device__ __forceinline__ long long tri_l(long long j, long long p) {
   return ((j * (j + 1)) >> 1) + p;  // lower triangle: row j holds p = 0..j
 }
 
@@ -86,7 +89,6 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
   const int row = q - nip;
   const int len = isip ? M : M - row;
   const int b0q = a.b0[q];
-  const int cnt = b0q < len ? b0q : len;
   const double dlq = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[row];
   const double INF = dinf();
   double* gE = isip ? a.ipres : a.G + tri_u(row, row, M);
@@ -99,29 +101,33 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
   bool num_ok = true;
 #pragma unroll
   for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(a.P.prefix[n]);
-  for (int base = 0; base < cnt; base += 32) {
+  // regular chains b < b0, 32 per pass, in b order; a chain is dropped once
+  // a user is infeasible or its offloader count exceeds b (it never
+  // decreases), and a pass ends when all its chains are dropped
+  const int creg = b0q - 1 < len ? b0q - 1 : len;
+  for (int base = 0; base < creg; base += 32) {
     const int b = base + lane + 1;
-    bool alive[1] = {b <= cnt};
-    const bool al[1] = {b == b0q};
-    const int kmin = isip ? M - 1 : (al[0] ? b0q - 1 : b - 1);
+    bool alive[1] = {b <= creg};
+    const bool al[1] = {false};
+    const int kmin = isip ? M - 1 : b - 1;
     double s[1][N], tot[1] = {0.0};
-    if (alive[0] && !al[0]) {
+    if (alive[0]) {
       start_times<N>(a.lat, a.P.bmax, dlq, b, s[0]);
     } else {
 #pragma unroll
       for (int n = 0; n < N; ++n) s[0][n] = -1.0;
     }
     int off = 0;
-    for (int kk = 0; kk < len; ++kk) {
+    for (int kk = 0; kk < len && __any_sync(kFull, alive[0]); ++kk) {
       if (alive[0]) {
         const int ri = isip ? a.rank[kk] : row + kk;
         int sp[1] = {0};
         const bool live[1] = {true};
         eval_multi<N, 1, SIMPLE>(a.rec + (size_t)ri * R::SIZE, a.P, s, al, num_ok, live, tot, sp);
-        alive[0] = sp[0] >= 0;
         off += (sp[0] >= 0 && sp[0] < N);
+        alive[0] = sp[0] >= 0 && off <= b;
       }
-      const bool cand = alive[0] && kk >= kmin && off <= b;
+      const bool cand = alive[0] && kk >= kmin;
       const unsigned long long key = (unsigned long long)__double_as_longlong(tot[0]);
       const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
       const unsigned mh = __reduce_min_sync(kFull, cand ? khi : 0xffffffffu);
@@ -135,12 +141,33 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
         const int slot = isip ? 0 : kk;
         if (tot[0] <= gE[slot]) {  // later passes carry larger b: they win ties
           gE[slot] = tot[0];
-          gB[slot] = (uint16_t)(al[0] ? kk + 1 : b);
+          gB[slot] = (uint16_t)b;
         }
       }
     }
     __syncwarp();
   }
+  // the all-local chain (every bound >= b0): each user runs local_only_choice
+  // at f_L, so a step is that user's N local fold terms; its key is the
+  // largest admissible bound (j-i+1, IP: M), larger than every regular b
+  if (b0q <= len && lane == 0) {
+    double t = 0.0;
+    for (int kk = 0; kk < len; ++kk) {
+      const double* r = a.rec + (size_t)(isip ? a.rank[kk] : row + kk) * R::SIZE;
+      if (r[R::FEAS] == 0.0) break;
+      const double fL = r[R::FL];
+#pragma unroll
+      for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __dmul_rn(__dmul_rn(r[R::KA(n)], fL), fL));
+      if (kk >= (isip ? M - 1 : b0q - 1)) {
+        const int slot = isip ? 0 : kk;
+        if (t <= gE[slot]) {
+          gE[slot] = t;
+          gB[slot] = (uint16_t)(isip ? M : kk + 1);
+        }
+      }
+    }
+  }
+  __syncwarp();
 }
 
 template <int N>
@@ -225,73 +252,60 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   if (!a.do_og) return;
 
   // ------------------------------------------------------------------ DP
-  for (int j = tid; j < M; j += NT) {  // S[0][j] = G[0][j]
-    a.St[tri_l(j, 0)] = a.G[tri_u(0, j, M)];
-    a.par[tri_l(j, 0)] = 0xffff;
+  // S[i][j] = min over feasible prev of fl(S[prev][i-1] + G[i][j]), smallest
+  // prev on ties: feasible prevs are the prefix [0, pfit) and the minimum
+  // is fl(PM + g) with PM the column prefix minimum; the parent is the first
+  // position of that minimum unless rounding merges an earlier, larger S
+  // (then a binary search).  PM/argpm of column j after stage i are the
+  // running values runPM[j]/runArg[j] (shared memory), written to row i.
+  double* runPM = PM;  // M doubles of shared memory
+  int* runArg = reinterpret_cast<int*>(gh + M);
+  double* PMg = a.St;  // upper triangle: PMg[tri_u(i, j)] = min_{q <= i} S[q][j]
+  for (int j = tid; j < M; j += NT) {  // row 0: S[0][j] = G[0][j]
+    const double g = a.G[tri_u(0, j, M)];
+    PMg[tri_u(0, j, M)] = g;
+    a.argpm[tri_u(0, j, M)] = 0;
+    a.par[tri_u(0, j, M)] = 0xffff;
+    runPM[j] = g;
+    runArg[j] = 0;
   }
+  if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
   __syncthreads();
   for (int i = 1; i < M; ++i) {
-    // prefix minimum of the column S[.][i-1] (contiguous in St row i-1)
-    const double* col = a.St + tri_l(i - 1, 0);
-    const int per = (i + NT - 1) / NT;  // consecutive elements per thread
-    const int p0 = tid * per;
-    double run = INF;
-    for (int p = p0; p < p0 + per && p < i; ++p) {
-      const double v = col[p];
-      if (v < run) run = v;
-      PM[p] = run;
-    }
-    // exclusive block scan (min) of the per-thread minima
-    double x = run;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double y = __shfl_up_sync(kFull, x, off);
-      if (lane >= off && y < x) x = y;
-    }
-    if (lane == 31) wred[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      double w = lane < NW ? wred[lane] : INF;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const double y = __shfl_up_sync(kFull, w, off);
-        if (lane >= off && y < w) w = y;
-      }
-      if (lane < NW) wred[lane] = w;
-    }
-    __syncthreads();
-    double carry = __shfl_up_sync(kFull, x, 1);
-    if (lane == 0) carry = INF;
-    if (warp > 0 && wred[warp - 1] < carry) carry = wred[warp - 1];
-    for (int p = p0; p < p0 + per && p < i; ++p)
-      if (carry < PM[p]) PM[p] = carry;
-    __syncthreads();
-    const double di = dls[i];
     for (int j = i + tid; j < M; j += NT) {
-      const double g = a.G[tri_u(i, j, M)];
-      const double sl = a.sumlat[j - i + 1];
-      int lo = 0, hi = i;  // P = #prevs with groups_fit (offline_solvers.hpp:229-232)
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__dadd_rn(dls[mid], sl) <= di) lo = mid + 1; else hi = mid;
-      }
-      double res = INF;
-      int pr = 0xffff;
-      if (g != INF && lo > 0) {
-        const double m = PM[lo - 1];
-        const double v = __dadd_rn(m, g);
-        if (m != INF && v < INF) {
-          int l2 = 0, h2 = lo - 1;  // first p with fl(PM[p] + g) <= v: the smallest prev
-          while (l2 < h2) {
-            const int mid = (l2 + h2) >> 1;
-            if (__dadd_rn(PM[mid], g) <= v) h2 = mid; else l2 = mid + 1;
+      const long long x = tri_u(i, j, M);
+      const double g = a.G[x];
+      const int p = a.pfit[x];
+      double best = INF;
+      int bp = 0xffff;
+      if (g != INF && p > 0) {
+        const long long cp = tri_u(p - 1, i - 1, M);
+        const double cand = __dadd_rn(PMg[cp], g);
+        if (cand != INF) {
+          best = cand;
+          int qb = a.argpm[cp];
+          // an earlier prev attains the same sum only if the prefix minimum
+          // before the first minimum position already does (monotone in q)
+          if (qb > 0 && __dadd_rn(PMg[tri_u(qb - 1, i - 1, M)], g) == best) {
+            int qa = 0;
+            --qb;
+            while (qa < qb) {
+              const int mid = (qa + qb) >> 1;
+              if (__dadd_rn(PMg[tri_u(mid, i - 1, M)], g) == best) qb = mid;
+              else qa = mid + 1;
+            }
           }
-          res = v;
-          pr = l2;
+          bp = qb;
         }
       }
-      a.St[tri_l(j, i)] = res;
-      a.par[tri_l(j, i)] = (uint16_t)pr;
+      if (j == M - 1) a.slast[i] = best;
+      a.par[x] = (uint16_t)bp;
+      if (best < runPM[j]) {  // strict: the first position is kept
+        runPM[j] = best;
+        runArg[j] = i;
+      }
+      PMg[x] = runPM[j];
+      a.argpm[x] = (uint16_t)runArg[j];
     }
     __syncthreads();
   }
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
     double bv = INF;
     int bi = M;
     for (int i = tid; i < M; i += NT) {
-      const double v = a.St[tri_l(M - 1, i)];
+      const double v = a.slast[i];
       if (v < bv || (v == bv && i < bi)) {
         bv = v;
         bi = i;
@@ -385,7 +399,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
       gh[ng] = j;
       ++ng;
       if (i == 0) break;
-      const int prev = a.par[tri_l(j, i)];
+      const int prev = a.par[tri_u(i, j, M)];
       j = i - 1;
       i = prev;
     }
@@ -460,8 +474,33 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
 size_t large_ws_bytes(int M, int N) {
   const size_t T = (size_t)M * (M + 1) / 2;
   const size_t rec = (size_t)M * rec_size(N) * 8;
-  // G, St (fp64) + bstar, par (u16) + records + dls/sumlat/fpos/genergy + ints
-  return 16 * T + 4 * T + rec + 8 * ((size_t)M + 2) * 4 + 4 * ((size_t)M + 2) * 5 + 4096 + 64 * 16;
+  // G, St (fp64) + bstar, par, pfit, argpm (u16) + records + dls/sumlat/fpos/genergy/slast + ints
+  return 16 * T + 8 * T + rec + 8 * ((size_t)M + 2) * 5 + 4 * ((size_t)M + 2) * 5 + 4096 + 64 * 16;
+}
+
+// Feasible-prev prefix length of every DP cell (i >= 1): the number of prevs
+// in [0, i) with groups_fit(dl[prev], dl[i], j-i+1) (offline_solvers.hpp:229-232).
+__global__ void large_pfit(LargeArgs a) {
+  const int M = a.M;
+  const long long T = (long long)M * (M + 1) / 2;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < T;
+       x += (long long)gridDim.x * blockDim.x) {
+    // row i of upper-triangle index x: largest i with tri_u(i, i) <= x
+    int lo = 0, hi = M - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tri_u(mid, mid, M) <= x) lo = mid; else hi = mid - 1;
+    }
+    const int i = lo, j = i + (int)(x - tri_u(i, i, M));
+    if (i == 0) continue;
+    const double thr = a.sumlat[j - i + 1], di = a.dls[i];
+    int l2 = 0, h2 = i;
+    while (l2 < h2) {
+      const int mid = (l2 + h2) >> 1;
+      if (__dadd_rn(a.dls[mid], thr) <= di) l2 = mid + 1; else h2 = mid;
+    }
+    a.pfit[x] = (uint16_t)l2;
+  }
 }
 
 __global__ void large_init(LargeArgs a) {
@@ -477,7 +516,9 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   large_prep<N><<<(M + 256) / 256, 256, 0, st>>>(a);
   large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
-  const int smem = 8 * 2 * M + 4 * 2 * M;
+  if (a.do_og) large_pfit<<<148 * 8, 256, 0, st>>>(a);
+  const int smem = 8 * 2 * M + 4 * 3 * M;  // dls, running PM | gl, gh, running argpm
+  if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
   cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   large_finish<N><<<1, 1024, smem, st>>>(a);
