@@ -15,7 +15,7 @@ namespace cfb {
 struct SmemLayout {
   int rec, tri, dls, sumlat, ipe, fsc;
   int rowoff, b0, order, rank, gid, glo, ghi, gitem, gbest, misc;
-  int pfit, argpm, parent, spsc, ipb;
+  int pfit, argpm, parent, spsc, ipb, lat;
   int total;
 };
 
