@@ -1,6 +1,8 @@
 // probe.cu — fp64-pipe throughput microbenchmark (roofline denominator).
 // Each thread runs 8 independent DFMA chains (no FMA contraction concerns:
-// this is a throughput probe, not a solver path).  ops = threads * iters * 8.
+// this is a throughput probe, not a solver path), full occupancy, loop
+// unrolled so loop overhead stays far below the fp64 pipe's issue share.
+// ops = threads * iters * 8; best of 5 launches of ~10 ms.
 #include <cuda_runtime.h>
 
 #include "../../include/coinfer_b200.h"
@@ -10,6 +12,7 @@ namespace cfb {
 __global__ void __launch_bounds__(256) dfma_probe(double* out, int iters, double a, double b) {
   double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
   double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+#pragma unroll 8
   for (int i = 0; i < iters; ++i) {
     x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b); x3 = __fma_rn(x3, a, b);
     x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b); x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
@@ -25,7 +28,8 @@ cudaError_t probe_fp64(cudaStream_t st, double* ops_per_s) {
   double* out = nullptr;
   cudaError_t e = cudaMalloc(&out, 8);
   if (e != cudaSuccess) return e;
-  const int blocks = sms * 8, threads = 256, iters = 4096;
+  // ~10 ms per launch at full occupancy, so ramp-up and tail are < 1%
+  const int blocks = sms * 8, threads = 256, iters = 65536;
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
