@@ -285,6 +285,7 @@ int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st)
   L.b0 = reinterpret_cast<int*>(take(4 * ((size_t)M + 2)));
   L.spos = reinterpret_cast<int*>(take(4 * (size_t)M));
   L.gid = reinterpret_cast<int*>(take(4 * (size_t)M));
+  L.rlen = reinterpret_cast<int*>(take(4 * (size_t)M));
   L.status = reinterpret_cast<int*>(take(4));
   L.simple = reinterpret_cast<int*>(take(4));
   L.ipb = reinterpret_cast<uint16_t*>(take(4));

@@ -75,7 +75,7 @@ struct LargeArgs {
   int* status;  // INT_MAX, or the first failing user * 32 + code
   int* simple;  // all arrivals and f_min zero
   double *rec, *dls, *sumlat, *G, *St, *ipres, *fpos, *genergy, *slast;
-  int *order, *rank, *b0, *spos, *gid;
+  int *order, *rank, *b0, *spos, *gid, *rlen;
   uint16_t *bstar, *par, *ipb, *pfit, *argpm;
   coinfer_ipssa_out ip;
   coinfer_og_out og;

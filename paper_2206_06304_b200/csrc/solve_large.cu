@@ -79,6 +79,22 @@ __global__ void large_rows(LargeArgs a) {
   const int len = isip ? M : M - (q - nip);
   const double d = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[q - nip];
   a.b0[q] = first_infeasible<N>(a.lat, a.P.bmax, d, len);
+  if (!isip) {
+    // useful length (solve_core.cuh, "Useful cells"): cells (row, j) with
+    // dl[0] + sumlat(j-row+1) > dl[row] have no fitting prev, so the DP
+    // never reads their G; the row's chains stop before them and bounds
+    // b > rlen do not run
+    const int row = q - nip;
+    int lo = 0, hi = len;
+    if (row > 0)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__dadd_rn(a.dls[0], a.sumlat[mid]) <= d) lo = mid; else hi = mid - 1;
+      }
+    else
+      lo = len;
+    a.rlen[row] = lo;
+  }
 }
 
 template <int N, bool SIMPLE>
@@ -101,10 +117,11 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
   bool num_ok = true;
 #pragma unroll
   for (int n = 1; n < N; ++n) num_ok = num_ok && numerator_fast_ok(a.P.prefix[n]);
+  const int rl = isip ? M : a.rlen[row];  // useful length (large_rows)
   // regular chains b < b0, 32 per pass, in b order; a chain is dropped once
   // a user is infeasible or its offloader count exceeds b (it never
   // decreases), and a pass ends when all its chains are dropped
-  const int creg = b0q - 1 < len ? b0q - 1 : len;
+  const int creg = b0q - 1 < rl ? b0q - 1 : rl;
   for (int base = 0; base < creg; base += 32) {
     const int b = base + lane + 1;
     bool alive[1] = {b <= creg};
@@ -118,7 +135,7 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
       for (int n = 0; n < N; ++n) s[0][n] = -1.0;
     }
     int off = 0;
-    for (int kk = 0; kk < len && __any_sync(kFull, alive[0]); ++kk) {
+    for (int kk = 0; kk < rl && __any_sync(kFull, alive[0]); ++kk) {
       if (alive[0]) {
         const int ri = isip ? a.rank[kk] : row + kk;
         int sp[1] = {0};
@@ -150,9 +167,9 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
   // the all-local chain (every bound >= b0): each user runs local_only_choice
   // at f_L, so a step is that user's N local fold terms; its key is the
   // largest admissible bound (j-i+1, IP: M), larger than every regular b
-  if (b0q <= len && lane == 0) {
+  if (b0q <= rl && lane == 0) {
     double t = 0.0;
-    for (int kk = 0; kk < len; ++kk) {
+    for (int kk = 0; kk < rl; ++kk) {
       const double* r = a.rec + (size_t)(isip ? a.rank[kk] : row + kk) * R::SIZE;
       if (r[R::FEAS] == 0.0) break;
       const double fL = r[R::FL];
@@ -272,10 +289,12 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
   __syncthreads();
   for (int i = 1; i < M; ++i) {
+    const int rli = a.rlen[i];
     for (int j = i + tid; j < M; j += NT) {
       const long long x = tri_u(i, j, M);
-      const double g = a.G[x];
-      const int p = a.pfit[x];
+      const bool use = j - i < rli;  // else no prev fits (pfit 0): S = +inf
+      const double g = use ? a.G[x] : INF;
+      const int p = use ? a.pfit[x] : 0;
       double best = INF;
       int bp = 0xffff;
       if (g != INF && p > 0) {
@@ -474,8 +493,9 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
 size_t large_ws_bytes(int M, int N) {
   const size_t T = (size_t)M * (M + 1) / 2;
   const size_t rec = (size_t)M * rec_size(N) * 8;
-  // G, St (fp64) + bstar, par, pfit, argpm (u16) + records + dls/sumlat/fpos/genergy/slast + ints
-  return 16 * T + 8 * T + rec + 8 * ((size_t)M + 2) * 5 + 4 * ((size_t)M + 2) * 5 + 4096 + 64 * 16;
+  // G, St (fp64) + bstar, par, pfit, argpm (u16) + records + dls/sumlat/fpos/genergy/slast + 6 int arrays
+  // (every take() rounds up to 256 bytes: 32 * 256 covers all of them)
+  return 16 * T + 8 * T + rec + 8 * ((size_t)M + 2) * 5 + 4 * ((size_t)M + 2) * 6 + 32 * 256;
 }
 
 // Feasible-prev prefix length of every DP cell (i >= 1): the number of prevs
@@ -494,7 +514,7 @@ __global__ void large_pfit(LargeArgs a) {
     const int i = lo, j = i + (int)(x - tri_u(i, i, M));
     if (i == 0) continue;
     const double thr = a.sumlat[j - i + 1], di = a.dls[i];
-    int l2 = 0, h2 = i;
+    int l2 = 0, h2 = __dadd_rn(a.dls[0], thr) <= di ? i : 0;  // no prev fits: 0
     while (l2 < h2) {
       const int mid = (l2 + h2) >> 1;
       if (__dadd_rn(a.dls[mid], thr) <= di) l2 = mid + 1; else h2 = mid;
