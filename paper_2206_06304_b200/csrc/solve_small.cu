@@ -20,17 +20,20 @@
 //    pipeline does not fit dl[i] all give the same all-local plan, so they
 //    collapse into one "all-local" chain keyed with the largest admissible b.
 //    The IP-SSA solve is one more chain set over the users in original order.
-//  * All chains of the instance are laid out flat (IP chains, then row 0,
-//    row 1, ... with b ascending) and cut into warp tasks of 32 lanes, so
-//    lanes stay ~98% busy.  After every step j each row segment of a warp
-//    takes a segmented lexicographic argmin over its lanes (energy asc, b
-//    desc == the reference's descending-b scan with strict '<').  A row that
-//    continues from a task running concurrently writes into a per-warp head
-//    buffer that is merged (in b order) after the round barrier.
-//  * The grouping DP runs in place over the G triangle (S[i][j] replaces
-//    G[i][j]); each stage is a lexicographic (value, prev) min over
-//    (j, prev) pairs split across the CTA.  Backtrack, then every chosen
-//    group is re-derived from its stored b to produce per-user outputs.
+//  * A chain dies once its offloader count exceeds b (it never decreases),
+//    and OG rows stop at their last cell the DP can read (a cell no group
+//    fits before has S = +inf whatever G holds).
+//  * Chains are dealt to 4-lane slots in chunks of one row; a slot steps
+//    its row's users together (one broadcast record read) and merges its
+//    candidates into the G cell with an order-free 64-bit min.  The bound
+//    attaining each chosen cell (the reference's descending-b scan with
+//    strict '<') is re-derived only for the groups the DP picks.
+//  * The grouping DP runs in place over the G triangle: per cell, the
+//    feasible prevs are a prefix (binary search before the G phase) and the
+//    minimum over them is a column prefix minimum kept in the triangle,
+//    one barrier per stage.  Backtrack, b*, then every chosen group is
+//    re-derived to produce the per-user outputs.
+//  See solve_core.cuh for the details and DESIGN.md §2 for the proofs.
 
 #include "solve_core.cuh"
 
