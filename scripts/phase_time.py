@@ -13,10 +13,10 @@ lib = _abi.load_library()
 lib.coinfer_debug_phase_cycles(buf, 1)
 eng.sweep(prof, dev); torch.cuda.synchronize()
 lib.coinfer_debug_phase_cycles(buf, 1)
-names = ["check/sort/hoist/rows", "G table", "IP-SSA out", "DP", "backtrack/b*/stitch"]
-tot = sum(buf[:5])
-for i, n in enumerate(names):
-    print(f"{n:24s} {buf[i]/K:12.0f} cycles/instance  {buf[i]/tot*100:5.1f}%")
+names = ["rows/pools/pfit", "G table", "IP-SSA out", "DP", "backtrack/b*/stitch", "check/sort/hoist"]
+tot = sum(buf[:6])
+for i in [5, 0, 1, 2, 3, 4]:
+    print(f"{names[i]:24s} {buf[i]/K:12.0f} cycles/instance  {buf[i]/tot*100:5.1f}%")
 if buf[7]:
     print(f"G phase: {buf[6]/K:.0f} active lane-steps/instance, {buf[7]/K:.0f} warp-steps/instance, "
           f"lane utilisation {buf[6]/(32*buf[7])*100:.1f}%")
