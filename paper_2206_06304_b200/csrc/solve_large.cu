@@ -206,10 +206,16 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   extern __shared__ __align__(16) unsigned char smb[];
   const int M = a.M, nip = a.do_ip ? 1 : 0;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
-  double* dls = reinterpret_cast<double*>(smb);
-  double* PM = dls + M;
-  int* gl = reinterpret_cast<int*>(PM + M);
+  // shared memory: DP running column minima + the cached column i-1;
+  // after the DP the group bounds reuse the column cache
+  double* runPM = reinterpret_cast<double*>(smb);  // [M]
+  double* colV = runPM + M;                        // [M]
+  int* ccount = reinterpret_cast<int*>(colV + M);  // [M]
+  int* colR = ccount + M;                          // [M]
+  int* rlenS = colR + M;                           // [M] useful row lengths
+  int* gl = reinterpret_cast<int*>(colV);  // after the DP
   int* gh = gl + M;
+  const double* dls = a.dls;
   __shared__ double wred[32];
   __shared__ int ired[32];
   __shared__ int s_best, s_ng, s_st;
@@ -223,9 +229,6 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
     }
     return;
   }
-  for (int x = tid; x < M; x += NT) dls[x] = a.dls[x];
-  __syncthreads();
-
   // ------------------------------------------------------------- IP-SSA out
   if (a.do_ip) {
     const double ipE = a.ipres[0];
@@ -273,61 +276,121 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   // prev on ties: feasible prevs are the prefix [0, pfit) and the minimum
   // is fl(PM + g) with PM the column prefix minimum; the parent is the first
   // position of that minimum unless rounding merges an earlier, larger S
-  // (then a binary search).  PM/argpm of column j after stage i are the
-  // running values runPM[j]/runArg[j] (shared memory), written to row i.
-  double* runPM = PM;  // M doubles of shared memory
-  int* runArg = reinterpret_cast<int*>(gh + M);
-  double* PMg = a.St;  // upper triangle: PMg[tri_u(i, j)] = min_{q <= i} S[q][j]
+  // into the same sum (then the earliest such position).  A column's prefix
+  // minimum is a step function of the row that drops only where S sets a
+  // new strict minimum, so each column keeps just its change points (row,
+  // value) -- about ln(M) of them -- appended in global memory (column c
+  // at c(c+1)/2, the worst case fits).  Stage i loads the finished column
+  // i-1's change points into shared memory; PM(p-1) is the last change
+  // point at a row <= p-1, its row is the first position of the minimum,
+  // and earlier rows with the same sum are earlier change points (binary
+  // searches over a handful of entries).  Cells past a row's useful length
+  // have no fitting prev (pfit 0).
+  double* chgV = a.St;
+  uint16_t* chgR = a.argpm;
+  auto coff = [](int c) { return (long long)c * (c + 1) / 2; };
+  for (int j = tid; j < M; j += NT) rlenS[j] = a.rlen[j];
   for (int j = tid; j < M; j += NT) {  // row 0: S[0][j] = G[0][j]
     const double g = a.G[tri_u(0, j, M)];
-    PMg[tri_u(0, j, M)] = g;
-    a.argpm[tri_u(0, j, M)] = 0;
-    a.par[tri_u(0, j, M)] = 0xffff;
     runPM[j] = g;
-    runArg[j] = 0;
+    ccount[j] = g < INF ? 1 : 0;
+    if (g < INF) {
+      chgV[coff(j)] = g;
+      chgR[coff(j)] = 0;
+    }
+    a.par[tri_u(0, j, M)] = 0xffff;
   }
   if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
   __syncthreads();
-  for (int i = 1; i < M; ++i) {
-    const int rli = a.rlen[i];
-    for (int j = i + tid; j < M; j += NT) {
-      const long long x = tri_u(i, j, M);
-      const bool use = j - i < rli;  // else no prev fits (pfit 0): S = +inf
-      const double g = use ? a.G[x] : INF;
-      const int p = use ? a.pfit[x] : 0;
-      double best = INF;
-      int bp = 0xffff;
-      if (g != INF && p > 0) {
-        const long long cp = tri_u(p - 1, i - 1, M);
-        const double cand = __dadd_rn(PMg[cp], g);
+  // one DP cell (i, j) with its G value and pfit, column i-1 in colV/colR
+  auto cell = [&](int i, int j, long long x, double g, int p, int nc) {
+    double best = INF;
+    int bp = 0xffff;
+    if (g != INF && p > 0) {
+      int lo = 0, hi = nc;  // change points at rows <= p-1
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (colR[mid] <= p - 1) lo = mid + 1; else hi = mid;
+      }
+      if (lo > 0) {
+        int k = lo - 1;
+        const double cand = __dadd_rn(colV[k], g);
         if (cand != INF) {
           best = cand;
-          int qb = a.argpm[cp];
-          // an earlier prev attains the same sum only if the prefix minimum
-          // before the first minimum position already does (monotone in q)
-          if (qb > 0 && __dadd_rn(PMg[tri_u(qb - 1, i - 1, M)], g) == best) {
-            int qa = 0;
-            --qb;
-            while (qa < qb) {
-              const int mid = (qa + qb) >> 1;
-              if (__dadd_rn(PMg[tri_u(mid, i - 1, M)], g) == best) qb = mid;
-              else qa = mid + 1;
+          if (k > 0 && __dadd_rn(colV[k - 1], g) == best) {  // rounding merged earlier minima
+            int ka = 0;
+            --k;
+            while (ka < k) {
+              const int mid = (ka + k) >> 1;
+              if (__dadd_rn(colV[mid], g) == best) k = mid; else ka = mid + 1;
             }
           }
-          bp = qb;
+          bp = colR[k];
         }
       }
-      if (j == M - 1) a.slast[i] = best;
-      a.par[x] = (uint16_t)bp;
-      if (best < runPM[j]) {  // strict: the first position is kept
-        runPM[j] = best;
-        runArg[j] = i;
+    }
+    if (j == M - 1) a.slast[i] = best;
+    a.par[x] = (uint16_t)bp;
+    if (best < runPM[j]) {  // strict: the first position is kept
+      runPM[j] = best;
+      const int n = ccount[j]++;
+      chgV[coff(j) + n] = best;
+      chgR[coff(j) + n] = (uint16_t)i;
+    }
+  };
+  // Only a row's useful cells j < i + rlen[i] are computed: past them no
+  // prev fits, S = +inf changes no running minimum and no parent is ever
+  // followed.  Rows of <= 64 useful cells (almost all of them on C4, where
+  // rlen averages ~35) run on warp 0 alone, synchronised by __syncwarp; the
+  // other warps skip ahead to the next long row, which runs on the whole
+  // CTA between barriers (<= 8 cells per thread since M <= 8*NT).  A cell's
+  // G and pfit loads are issued before, and overlap, the column load.
+  for (int i = 1; i < M; ++i) {
+    const int jend = i + rlenS[i];
+    const long long xr = tri_u(i, i, M) - i;  // x(i, j) = xr + j
+    const long long c0 = coff(i - 1);
+    if (jend - i <= 64) {
+      if (warp != 0) continue;
+      const int nc = ccount[i - 1];
+      if (lane == 0 && jend < M) a.slast[i] = INF;
+      const int ja = i + lane, jb = i + 32 + lane;
+      const double ga = ja < jend ? a.G[xr + ja] : INF, gb = jb < jend ? a.G[xr + jb] : INF;
+      const int pa = ja < jend ? a.pfit[xr + ja] : 0, pb = jb < jend ? a.pfit[xr + jb] : 0;
+      for (int q = lane; q < nc; q += 32) {
+        colV[q] = chgV[c0 + q];
+        colR[q] = chgR[c0 + q];
       }
-      PMg[x] = runPM[j];
-      a.argpm[x] = (uint16_t)runArg[j];
+      __syncwarp();
+      if (ja < jend) cell(i, ja, xr + ja, ga, pa, nc);
+      if (jb < jend) cell(i, jb, xr + jb, gb, pb, nc);
+      __syncwarp();
+      continue;
+    }
+    __syncthreads();  // warp 0's short rows are done
+    const int nc = ccount[i - 1];
+    if (tid == 0 && jend < M) a.slast[i] = INF;
+    double gv[8];
+    int pv[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = i + tid + c * NT;
+      gv[c] = j < jend ? a.G[xr + j] : INF;
+      pv[c] = j < jend ? a.pfit[xr + j] : 0;
+    }
+    for (int q = tid; q < nc; q += NT) {
+      colV[q] = chgV[c0 + q];
+      colR[q] = chgR[c0 + q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = i + tid + c * NT;
+      if (j >= jend) break;
+      cell(i, j, xr + j, gv[c], pv[c], nc);
     }
     __syncthreads();
   }
+  __syncthreads();
 
   // best_i: strict '<', smallest i (offline_solvers.hpp:332-334); S[i][M-1] = St row M-1
   {
@@ -537,7 +600,7 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
   if (a.do_og) large_pfit<<<148 * 8, 256, 0, st>>>(a);
-  const int smem = 8 * 2 * M + 4 * 3 * M;  // dls, running PM | gl, gh, running argpm
+  const int smem = 8 * 2 * M + 4 * 3 * M;  // running PM, column change values | counts, change rows, rlen
   if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
   cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -26,6 +26,23 @@ def test_large_vs_oracle(engine, M):
     ck.assert_same_og(og, ck.oracle_og(prof, users), where="large og")
 
 
+def test_large_loose_deadlines(engine):
+    """Loose deadlines: many rows keep more than 64 useful cells, so the DP
+    runs its whole-CTA stages as well as the single-warp ones."""
+    M = 300
+    prof = profile_heavy(M)
+    users = sample_batch(2, M, prof, 0.5, 3.0, seed=11)
+    sl = np.zeros(M + 1)
+    for n in range(prof.N):
+        sl[1:] = sl[1:] + prof.latency[n][:M]
+    dl = np.sort(users["deadline"][0])
+    rlen = [int(np.sum(dl[0] + sl[1:M - i + 1] <= dl[i])) for i in range(1, M)]
+    assert sum(r > 64 for r in rlen) > 50 and sum(r <= 64 for r in rlen) > 50
+    ip, og = engine.sweep(prof, users)
+    ck.assert_same_ip(ip, ck.oracle_ipssa(prof, users), where="large loose ipssa")
+    ck.assert_same_og(og, ck.oracle_og(prof, users), where="large loose og")
+
+
 def test_large_light_profile(engine):
     prof = profile_light(400)
     users = sample_batch(1, 400, prof, 0.05, 0.2, seed=5)
