@@ -15,9 +15,10 @@ the job.
          ranks.  Inputs (2.8 GB) exceed the 126 MB L2, so no flush is needed.
   e2e    the same solve through the C-ABI with HOST (pinned) buffers: H2D of
          the inputs, the solve, D2H of the decisions, every step.
-  roofline  fp64-pipe lane operations (SURVEY.md §8d work model) per launch
-         / launch time, against the fp64 throughput measured on this GPU by
-         coinfer_probe_fp64.
+  roofline  fp64-pipe lane operations per launch (SURVEY.md §8d per-unit
+         costs x the units the launch processes) / launch time, against the
+         fp64 throughput measured on this GPU by coinfer_probe_fp64; the §8d
+         count of the reference's own units is reported beside it.
   cpu_baseline  the reference C++ solvers (oracle/_ref, unmodified headers)
          on a bounded sample, all host threads, rank 0 at N=1.
 
@@ -347,14 +348,19 @@ def main():
             traffic = None
     w_pr = pruned_work_model(prof, users) + w_ip
     achieved_pr = w_pr / (ms * 1e-3)
-    roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "work_model": "SURVEY.md §8d: fp64-pipe lane ops, C_ub=19N-13, C_loc=3N+1, C_dp=4",
-                "ops_per_launch": w_og + w_ip,
-                "pruned": {"ops_per_launch": w_pr, "achieved": achieved_pr / 1e12,
-                           "frac": achieved_pr / peak,
-                           "note": "same formulas over the OG rows the DP can read (rlen-truncated, "
-                                   "DESIGN.md §3); the work this kernel must do, so its efficiency"},
+    roofline = {"bound": "fp64", "achieved": achieved_pr / 1e12, "peak": peak / 1e12,
+                "unit": "TFLOP/s", "frac": achieved_pr / peak, "traffic": traffic,
+                "work_model": "SURVEY.md §8d per-unit costs (fp64-pipe lane ops, C_ub=19N-13, "
+                              "C_loc=3N+1, C_dp=4) x the units this launch processes: the OG rows "
+                              "truncated to their DP-readable length rlen(i), bounds b <= rlen(i), "
+                              "every chain credited with its full truncated row (DESIGN.md §4)",
+                "ops_per_launch": w_pr,
+                "reference_work": {"ops_per_launch": w_og + w_ip, "achieved": achieved / 1e12,
+                                   "frac": achieved / peak,
+                                   "note": "SURVEY.md §8d W_OG + W_IPSSA: the reference algorithm's "
+                                           "units (every row to M-i users); the launch skips the "
+                                           "rows' unreadable tails exactly, so this rate exceeds "
+                                           "the fp64 peak"},
                 "peak_source": "coinfer_probe_fp64 on this GPU (8 independent DFMA chains/thread, burst)"}
 
     # ---------------- end to end through the C-ABI, host buffers ----------------
