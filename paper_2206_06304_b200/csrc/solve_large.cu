@@ -208,11 +208,16 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
   // shared memory: DP running column minima + the cached column i-1;
   // after the DP the group bounds reuse the column cache
-  double* runPM = reinterpret_cast<double*>(smb);  // [M]
-  double* colV = runPM + M;                        // [M]
-  int* ccount = reinterpret_cast<int*>(colV + M);  // [M]
-  int* colR = ccount + M;                          // [M]
-  int* rlenS = colR + M;                           // [M] useful row lengths
+  constexpr int RING = 128, CAP = 16;  // shared-memory mirror of recent columns (DP)
+  double* runPM = reinterpret_cast<double*>(smb);        // [M] running column minima
+  double* colV = runPM + M;                               // [M] a column staged from global
+  double* ringV = colV + M;                               // [RING*CAP]
+  int* ringOwn = reinterpret_cast<int*>(ringV + RING * CAP);  // [RING]
+  uint16_t* ringR = reinterpret_cast<uint16_t*>(ringOwn + RING);  // [RING*CAP]
+  uint16_t* ccount = ringR + RING * CAP;                  // [M] change points per column
+  uint16_t* colR = ccount + M;                            // [M]
+  uint16_t* rlenS = colR + M;                             // [M] useful row lengths
+  uint16_t* runRow = rlenS + M;                           // [M] row of the last change point
   int* gl = reinterpret_cast<int*>(colV);  // after the DP
   int* gh = gl + M;
   const double* dls = a.dls;
@@ -286,13 +291,22 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   // and earlier rows with the same sum are earlier change points (binary
   // searches over a handful of entries).  Cells past a row's useful length
   // have no fitting prev (pfit 0).
+  //   Change points always go to global memory (chgV/chgR, complete); a
+  // column whose first change after row 0 comes in a short-row stage also
+  // gets a slot in a shared-memory ring (column c in slot c % 128, up to 16
+  // points, claimed only once the slot's previous column has been read), so
+  // stage i usually finds column i-1 in shared memory: in the ring, or --
+  // when it has a single change point -- in runPM/runRow.  Only a column
+  // that overflowed or missed the ring is staged from global memory.
   double* chgV = a.St;
   uint16_t* chgR = a.argpm;
   auto coff = [](int c) { return (long long)c * (c + 1) / 2; };
-  for (int j = tid; j < M; j += NT) rlenS[j] = a.rlen[j];
+  for (int r = tid; r < RING; r += NT) ringOwn[r] = -1;
+  for (int j = tid; j < M; j += NT) rlenS[j] = (uint16_t)a.rlen[j];
   for (int j = tid; j < M; j += NT) {  // row 0: S[0][j] = G[0][j]
     const double g = a.G[tri_u(0, j, M)];
     runPM[j] = g;
+    runRow[j] = 0;
     ccount[j] = g < INF ? 1 : 0;
     if (g < INF) {
       chgV[coff(j)] = g;
@@ -302,67 +316,127 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   }
   if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
   __syncthreads();
-  // one DP cell (i, j) with its G value and pfit, column i-1 in colV/colR
-  auto cell = [&](int i, int j, long long x, double g, int p, int nc) {
+  // S[i][j] for cell (i, j) given G, pfit and column i-1's change points
+  // (V, Rr, nc); appends (i, S) to column j when it is a new strict minimum
+  // (`claim`: short-row stages, whose <= 64 columns are distinct mod RING)
+  auto cell = [&](int i, int j, long long x, double g, int p, const double* V, const uint16_t* Rr, int nc,
+                  bool claim) {
     double best = INF;
     int bp = 0xffff;
     if (g != INF && p > 0) {
       int lo = 0, hi = nc;  // change points at rows <= p-1
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (colR[mid] <= p - 1) lo = mid + 1; else hi = mid;
+        if (Rr[mid] <= p - 1) lo = mid + 1; else hi = mid;
       }
       if (lo > 0) {
         int k = lo - 1;
-        const double cand = __dadd_rn(colV[k], g);
+        const double cand = __dadd_rn(V[k], g);
         if (cand != INF) {
           best = cand;
-          if (k > 0 && __dadd_rn(colV[k - 1], g) == best) {  // rounding merged earlier minima
+          if (k > 0 && __dadd_rn(V[k - 1], g) == best) {  // rounding merged earlier minima
             int ka = 0;
             --k;
             while (ka < k) {
               const int mid = (ka + k) >> 1;
-              if (__dadd_rn(colV[mid], g) == best) k = mid; else ka = mid + 1;
+              if (__dadd_rn(V[mid], g) == best) k = mid; else ka = mid + 1;
             }
           }
-          bp = colR[k];
+          bp = Rr[k];
         }
       }
     }
     if (j == M - 1) a.slast[i] = best;
     a.par[x] = (uint16_t)bp;
     if (best < runPM[j]) {  // strict: the first position is kept
-      runPM[j] = best;
-      const int n = ccount[j]++;
+      const int n = ccount[j];
       chgV[coff(j) + n] = best;
       chgR[coff(j) + n] = (uint16_t)i;
+      const int slot = j & (RING - 1), own = ringOwn[slot];
+      double* rv = ringV + slot * CAP;
+      uint16_t* rr = ringR + slot * CAP;
+      if (own == j) {
+        if (n < CAP) {
+          rv[n] = best;
+          rr[n] = (uint16_t)i;
+        } else {
+          ringOwn[slot] = -1;  // overflow: the column is read from global memory
+        }
+      } else if (claim && n <= 1 && own < i - 1) {  // free, or its column already read
+        if (n == 1) {
+          rv[0] = runPM[j];
+          rr[0] = runRow[j];
+        }
+        rv[n] = best;
+        rr[n] = (uint16_t)i;
+        ringOwn[slot] = j;
+      }
+      ccount[j] = (uint16_t)(n + 1);
+      runPM[j] = best;
+      runRow[j] = (uint16_t)i;
     }
+  };
+  // column c's change points in shared memory, or nullptr (stage them from global)
+  auto column = [&](int c, int nc, const double*& V, const uint16_t*& Rr) {
+    if (nc <= 1) {
+      V = runPM + c;
+      Rr = runRow + c;
+      return true;
+    }
+    if (ringOwn[c & (RING - 1)] == c) {
+      V = ringV + (c & (RING - 1)) * CAP;
+      Rr = ringR + (c & (RING - 1)) * CAP;
+      return true;
+    }
+    V = colV;
+    Rr = colR;
+    return false;
   };
   // Only a row's useful cells j < i + rlen[i] are computed: past them no
   // prev fits, S = +inf changes no running minimum and no parent is ever
   // followed.  Rows of <= 64 useful cells (almost all of them on C4, where
-  // rlen averages ~35) run on warp 0 alone, synchronised by __syncwarp; the
-  // other warps skip ahead to the next long row, which runs on the whole
-  // CTA between barriers (<= 8 cells per thread since M <= 8*NT).  A cell's
-  // G and pfit loads are issued before, and overlap, the column load.
+  // rlen averages ~35) run on warp 0 alone, synchronised by __syncwarp, with
+  // the next row's G and pfit loads in flight; the other warps skip ahead to
+  // the next long row, which runs on the whole CTA between barriers (<= 8
+  // cells per thread since M <= 8*NT).
+  int pref = -1;  // warp 0: the row whose first 64 cells ga/gb, pa/pb hold
+  double ga = INF, gb = INF;
+  int pa = 0, pb = 0;
+  auto prefetch = [&](int r) {
+    const int je = r + rlenS[r];
+    const long long xr = tri_u(r, r, M) - r;
+    const int ja = r + lane, jb = r + 32 + lane;
+    ga = ja < je ? a.G[xr + ja] : INF;
+    gb = jb < je ? a.G[xr + jb] : INF;
+    pa = ja < je ? a.pfit[xr + ja] : 0;
+    pb = jb < je ? a.pfit[xr + jb] : 0;
+    pref = r;
+  };
   for (int i = 1; i < M; ++i) {
-    const int jend = i + rlenS[i];
+    const int rl = rlenS[i];
+    if (rl <= 64 && warp != 0) continue;  // short row: warp 0's
+    const int jend = i + rl;
     const long long xr = tri_u(i, i, M) - i;  // x(i, j) = xr + j
     const long long c0 = coff(i - 1);
-    if (jend - i <= 64) {
-      if (warp != 0) continue;
-      const int nc = ccount[i - 1];
+    if (rl <= 64) {
+      if (pref != i) prefetch(i);
+      const double g0 = ga, g1 = gb;
+      const int p0 = pa, p1 = pb;
+      if (i + 1 < M) prefetch(i + 1);  // in flight during this stage
       if (lane == 0 && jend < M) a.slast[i] = INF;
-      const int ja = i + lane, jb = i + 32 + lane;
-      const double ga = ja < jend ? a.G[xr + ja] : INF, gb = jb < jend ? a.G[xr + jb] : INF;
-      const int pa = ja < jend ? a.pfit[xr + ja] : 0, pb = jb < jend ? a.pfit[xr + jb] : 0;
-      for (int q = lane; q < nc; q += 32) {
-        colV[q] = chgV[c0 + q];
-        colR[q] = chgR[c0 + q];
+      const int nc = ccount[i - 1];
+      const double* V;
+      const uint16_t* Rr;
+      if (!column(i - 1, nc, V, Rr)) {
+        for (int q = lane; q < nc; q += 32) {
+          colV[q] = chgV[c0 + q];
+          colR[q] = chgR[c0 + q];
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (ja < jend) cell(i, ja, xr + ja, ga, pa, nc);
-      if (jb < jend) cell(i, jb, xr + jb, gb, pb, nc);
+      const int ja = i + lane, jb = i + 32 + lane;
+      if (ja < jend) cell(i, ja, xr + ja, g0, p0, V, Rr, nc, true);
+      if (jb < jend) cell(i, jb, xr + jb, g1, p1, V, Rr, nc, true);
       __syncwarp();
       continue;
     }
@@ -377,16 +451,19 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
       gv[c] = j < jend ? a.G[xr + j] : INF;
       pv[c] = j < jend ? a.pfit[xr + j] : 0;
     }
-    for (int q = tid; q < nc; q += NT) {
-      colV[q] = chgV[c0 + q];
-      colR[q] = chgR[c0 + q];
-    }
+    const double* V;
+    const uint16_t* Rr;
+    if (!column(i - 1, nc, V, Rr))
+      for (int q = tid; q < nc; q += NT) {
+        colV[q] = chgV[c0 + q];
+        colR[q] = chgR[c0 + q];
+      }
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int j = i + tid + c * NT;
       if (j >= jend) break;
-      cell(i, j, xr + j, gv[c], pv[c], nc);
+      cell(i, j, xr + j, gv[c], pv[c], V, Rr, nc, false);
     }
     __syncthreads();
   }
@@ -600,7 +677,8 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
   if (a.do_og) large_pfit<<<148 * 8, 256, 0, st>>>(a);
-  const int smem = 8 * 2 * M + 4 * 3 * M;  // running PM, column change values | counts, change rows, rlen
+  // running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
+  const int smem = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
   if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
   cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
