@@ -135,7 +135,21 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
       for (int n = 0; n < N; ++n) s[0][n] = -1.0;
     }
     int off = 0;
-    for (int kk = 0; kk < rl && __any_sync(kFull, alive[0]); ++kk) {
+    // the pass's winner for cell kk (the min energy, largest b on ties) is
+    // parked in lane kk % 32 and merged into the row 32 cells at a time
+    // (coalesced, off the per-step critical path)
+    double pv = INF;
+    int pb = 0;
+    auto flush = [&](int w0) {
+      const int cellk = w0 + lane;
+      if (pv != INF && cellk < rl && pv <= gE[cellk]) {  // later passes carry larger b: they win ties
+        gE[cellk] = pv;
+        gB[cellk] = (uint16_t)pb;
+      }
+      pv = INF;
+    };
+    int kk = 0;
+    for (; kk < rl && __any_sync(kFull, alive[0]); ++kk) {
       if (alive[0]) {
         const int ri = isip ? a.rank[kk] : row + kk;
         int sp[1] = {0};
@@ -154,34 +168,65 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
         const unsigned ml = __reduce_min_sync(kFull, hit ? klo : 0xffffffffu);
         wm = __ballot_sync(kFull, hit && klo == ml);
       }
-      if (wm != 0u && lane == 31 - __clz(wm)) {
-        const int slot = isip ? 0 : kk;
-        if (tot[0] <= gE[slot]) {  // later passes carry larger b: they win ties
-          gE[slot] = tot[0];
-          gB[slot] = (uint16_t)b;
+      if (isip) {
+        if (wm != 0u && lane == 31 - __clz(wm) && tot[0] <= gE[0]) {
+          gE[0] = tot[0];
+          gB[0] = (uint16_t)b;
         }
+        continue;
       }
+      const int win = 31 - __clz(wm);  // -1: no candidate
+      const double wv = __shfl_sync(kFull, tot[0], win & 31);
+      if (lane == (kk & 31) && wm != 0u) {
+        pv = wv;
+        pb = base + win + 1;
+      }
+      if ((kk & 31) == 31) flush(kk - 31);
     }
+    if (!isip && (kk & 31) != 0) flush(kk & ~31);
     __syncwarp();
   }
   // the all-local chain (every bound >= b0): each user runs local_only_choice
   // at f_L, so a step is that user's N local fold terms; its key is the
-  // largest admissible bound (j-i+1, IP: M), larger than every regular b
-  if (b0q <= rl && lane == 0) {
+  // largest admissible bound (j-i+1, IP: M), larger than every regular b.
+  // The fold stays one sequential sum; the warp computes 32 users' terms at
+  // a time, every lane runs the (identical) sum over them through shuffles
+  // and keeps the partial sum after its own user, then the 32 cells merge
+  // at once.
+  if (b0q <= rl) {
+    const int kmin = isip ? M - 1 : b0q - 1;
     double t = 0.0;
-    for (int kk = 0; kk < rl; ++kk) {
-      const double* r = a.rec + (size_t)(isip ? a.rank[kk] : row + kk) * R::SIZE;
-      if (r[R::FEAS] == 0.0) break;
-      const double fL = r[R::FL];
+    for (int c0 = 0; c0 < rl; c0 += 32) {
+      const int kk = c0 + lane;
+      double x[N];
+      bool feas = false;
+      if (kk < rl) {
+        const double* r = a.rec + (size_t)(isip ? a.rank[kk] : row + kk) * R::SIZE;
+        feas = r[R::FEAS] != 0.0;
+        const double fL = r[R::FL];
 #pragma unroll
-      for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __dmul_rn(__dmul_rn(r[R::KA(n)], fL), fL));
-      if (kk >= (isip ? M - 1 : b0q - 1)) {
+        for (int n = 1; n <= N; ++n) x[n - 1] = __dmul_rn(__dmul_rn(r[R::KA(n)], fL), fL);
+      } else {
+#pragma unroll
+        for (int n = 0; n < N; ++n) x[n] = 0.0;
+      }
+      // users up to the first one that cannot meet its deadline locally
+      const unsigned bad = __ballot_sync(kFull, kk < rl && !feas);
+      const int stop = bad ? __ffs(bad) - 1 : (rl - c0 < 32 ? rl - c0 : 32);
+      double mine = INF;
+      for (int u = 0; u < stop; ++u) {
+#pragma unroll
+        for (int n = 0; n < N; ++n) t = __dadd_rn(t, __shfl_sync(kFull, x[n], u));
+        if (lane == u) mine = t;
+      }
+      if (lane < stop && kk >= kmin) {
         const int slot = isip ? 0 : kk;
-        if (t <= gE[slot]) {
-          gE[slot] = t;
+        if (mine <= gE[slot]) {
+          gE[slot] = mine;
           gB[slot] = (uint16_t)(isip ? M : kk + 1);
         }
       }
+      if (bad) break;
     }
   }
   __syncwarp();
