@@ -188,9 +188,11 @@ static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid
 #ifdef CFB_PHASE_TIMING
 extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out + 8, g_ip_steps, sizeof(unsigned long long) * 2);
   if (reset) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+    cudaMemcpyToSymbol(g_ip_steps, z, sizeof(unsigned long long) * 2);
   }
   return 0;
 }

@@ -8,7 +8,7 @@ eng = Engine(0)
 prof = profile_heavy(50)
 dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, 50, prof, seed=1).items()}
 eng.sweep(prof, dev); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 10)()
 lib = _abi.load_library()
 lib.coinfer_debug_phase_cycles(buf, 1)
 eng.sweep(prof, dev); torch.cuda.synchronize()
@@ -20,3 +20,6 @@ for i in [5, 0, 1, 2, 3, 4]:
 if buf[7]:
     print(f"G phase: {buf[6]/K:.0f} active lane-steps/instance, {buf[7]/K:.0f} warp-steps/instance, "
           f"lane utilisation {buf[6]/(32*buf[7])*100:.1f}%")
+if buf[9]:
+    print(f"IP-SSA G loop: {buf[8]/K:.0f} active lane-steps/instance, {buf[9]/K:.0f} warp-steps/instance, "
+          f"lane utilisation {buf[8]/(32*buf[9])*100:.1f}%")
