@@ -245,6 +245,16 @@ __global__ void __launch_bounds__(128) large_grow(LargeArgs a) {
 }
 
 // One CTA: DP, backtrack, stitch, outputs (and the IP-SSA outputs).
+#ifndef CFB_LARGE_SHORT
+#define CFB_LARGE_SHORT 3  // DP rows of <= 32*this useful cells run on one warp
+#endif
+#ifdef CFB_LARGE_TIMING
+__device__ unsigned long long g_large_t[8];
+extern "C" int coinfer_debug_large_times(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_large_t, sizeof(unsigned long long) * 8);
+  return 0;
+}
+#endif
 template <int N>
 __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   using R = Rec<N>;
@@ -363,7 +373,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   __syncthreads();
   // S[i][j] for cell (i, j) given G, pfit and column i-1's change points
   // (V, Rr, nc); appends (i, S) to column j when it is a new strict minimum
-  // (`claim`: short-row stages, whose <= 64 columns are distinct mod RING)
+  // (`claim`: short-row stages, whose <= 96 columns are distinct mod RING)
   auto cell = [&](int i, int j, long long x, double g, int p, const double* V, const uint16_t* Rr, int nc,
                   bool claim) {
     double best = INF;
@@ -439,50 +449,78 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   };
   // Only a row's useful cells j < i + rlen[i] are computed: past them no
   // prev fits, S = +inf changes no running minimum and no parent is ever
-  // followed.  Rows of <= 64 useful cells (almost all of them on C4, where
-  // rlen averages ~35) run on warp 0 alone, synchronised by __syncwarp, with
+  // followed.  Rows of <= 96 useful cells (all of them on C4, where rlen
+  // averages ~35 and peaks in the 70s) run on warp 0 alone, synchronised by __syncwarp, with
   // the next row's G and pfit loads in flight; the other warps skip ahead to
   // the next long row, which runs on the whole CTA between barriers (<= 8
   // cells per thread since M <= 8*NT).
-  int pref = -1;  // warp 0: the row whose first 64 cells ga/gb, pa/pb hold
-  double ga = INF, gb = INF;
-  int pa = 0, pb = 0;
+  constexpr int SHORT = CFB_LARGE_SHORT;  // short rows: <= 32*SHORT useful cells
+  int pref = -1;  // warp 0: the row whose first 32*SHORT cells gq/pq hold
+  double gq[SHORT];
+  int pq[SHORT];
   auto prefetch = [&](int r) {
     const int je = r + rlenS[r];
     const long long xr = tri_u(r, r, M) - r;
-    const int ja = r + lane, jb = r + 32 + lane;
-    ga = ja < je ? a.G[xr + ja] : INF;
-    gb = jb < je ? a.G[xr + jb] : INF;
-    pa = ja < je ? a.pfit[xr + ja] : 0;
-    pb = jb < je ? a.pfit[xr + jb] : 0;
+#pragma unroll
+    for (int c = 0; c < SHORT; ++c) {
+      const int j = r + 32 * c + lane;
+      gq[c] = j < je ? a.G[xr + j] : INF;
+      pq[c] = j < je ? a.pfit[xr + j] : 0;
+    }
     pref = r;
   };
   for (int i = 1; i < M; ++i) {
     const int rl = rlenS[i];
-    if (rl <= 64 && warp != 0) continue;  // short row: warp 0's
+    if (rl <= 32 * SHORT && warp != 0) continue;  // short row: warp 0's
     const int jend = i + rl;
     const long long xr = tri_u(i, i, M) - i;  // x(i, j) = xr + j
     const long long c0 = coff(i - 1);
-    if (rl <= 64) {
+    if (rl <= 32 * SHORT) {
+#ifdef CFB_LARGE_TIMING
+      long long t0 = clock64();
+#endif
       if (pref != i) prefetch(i);
-      const double g0 = ga, g1 = gb;
-      const int p0 = pa, p1 = pb;
+      double gc[SHORT];
+      int pc[SHORT];
+#pragma unroll
+      for (int c = 0; c < SHORT; ++c) {
+        gc[c] = gq[c];
+        pc[c] = pq[c];
+      }
       if (i + 1 < M) prefetch(i + 1);  // in flight during this stage
       if (lane == 0 && jend < M) a.slast[i] = INF;
       const int nc = ccount[i - 1];
       const double* V;
       const uint16_t* Rr;
-      if (!column(i - 1, nc, V, Rr)) {
+      const bool insm = column(i - 1, nc, V, Rr);
+      if (!insm) {
         for (int q = lane; q < nc; q += 32) {
           colV[q] = chgV[c0 + q];
           colR[q] = chgR[c0 + q];
         }
         __syncwarp();
       }
-      const int ja = i + lane, jb = i + 32 + lane;
-      if (ja < jend) cell(i, ja, xr + ja, g0, p0, V, Rr, nc, true);
-      if (jb < jend) cell(i, jb, xr + jb, g1, p1, V, Rr, nc, true);
+#ifdef CFB_LARGE_TIMING
+      long long t1 = clock64();
+      const double gsink = gc[0] + (double)pc[0];
+      long long t2 = clock64();
+#endif
+#pragma unroll
+      for (int c = 0; c < SHORT; ++c) {
+        const int j = i + 32 * c + lane;
+        if (j < jend) cell(i, j, xr + j, gc[c], pc[c], V, Rr, nc, true);
+      }
       __syncwarp();
+#ifdef CFB_LARGE_TIMING
+      long long t3 = clock64();
+      if (lane == 0) {
+        g_large_t[0] += t1 - t0;
+        g_large_t[1] += t2 - t1 + (gsink == 12345.0);
+        g_large_t[2] += t3 - t2;
+        g_large_t[3] += 1;
+        g_large_t[4] += insm ? 0 : 1;
+      }
+#endif
       continue;
     }
     __syncthreads();  // warp 0's short rows are done
