@@ -99,6 +99,17 @@ def test_random_vs_oracle_sizes(engine, M):
         check_sweep(engine, prof, users)
 
 
+@pytest.mark.parametrize("M,lo,hi", [(150, 0.5, 3.0), (176, 0.5, 3.0), (176, 20.0, 40.0), (176, 0.25, 1.0), (255, 0.5, 3.0)])
+def test_small_path_largest_sizes(engine, M, lo, hi):
+    """The shared-memory path at its largest instances (M = 176, the largest
+    whose triangle fits in shared memory; 255 takes the large path): byte
+    row and chunk tables, useful lengths from a few cells up to whole rows
+    (loose deadlines: every group fits after every other)."""
+    prof = profile_heavy(M)
+    users = sample_batch(2, M, prof, lo, hi, seed=M)
+    check_sweep(engine, prof, users)
+
+
 @pytest.mark.parametrize("variant", ["fmin", "arrival", "equal", "tight", "loose", "flat", "N16"])
 def test_random_vs_oracle_variants(engine, variant):
     rng = np.random.default_rng(hash(variant) % 2**32)
