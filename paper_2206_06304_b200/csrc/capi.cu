@@ -371,9 +371,12 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   auto launch = [&](const cfb::SmallArgs& args, const int32_t* bd, size_t Kc, cudaStream_t st) {
     const int grid = (int)(Kc < (size_t)(1u << 30) ? Kc : (size_t)(1u << 30));
     if (mode == Mode::Fixed) return cfb::launch_fixed(args, bd, grid, st);
-    // Many instances: 4 warps per CTA and several CTAs per SM.  Few
-    // instances: 8 warps per CTA to spread each instance's chains wider.
-    const int threads = Kc >= 1024 ? 128 : 256;
+    // Many instances: 4 warps per CTA and several CTAs per SM.  Fewer: 8
+    // warps per CTA to spread each instance's chains wider; a handful (SMs
+    // would idle anyway): 16 warps per instance (measured best of 8/16/32 at
+    // M = 50..176; COINFER_WIDE overrides, for experiments).
+    static const int wide = std::getenv("COINFER_WIDE") ? std::atoi(std::getenv("COINFER_WIDE")) : 512;
+    const int threads = Kc >= 1024 ? 128 : Kc >= 148 ? 256 : wide;
     return cfb::launch_small(args, threads, grid, st);
   };
   static const bool force_large = std::getenv("COINFER_FORCE_LARGE") != nullptr;  // testing aid

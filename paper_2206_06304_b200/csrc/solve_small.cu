@@ -42,8 +42,12 @@ namespace cfb {
 
 int small_smem_bytes(int M, int N, int W) { return small_smem_bytes_impl(M, N, W); }
 
+// The batch kernel: up to 256 threads and several CTAs per SM (throughput),
+// or -- for a handful of instances, where SMs would idle -- one CTA of up to
+// 1024 threads per instance, so each instance's chains spread over more
+// lanes (latency).  Same body, same 64-register budget.
 template <int N>
-__global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallArgs a) {
+__device__ __forceinline__ void solve_batch(const SmallArgs& a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int M = a.M;
   for (int64_t k = blockIdx.x; k < a.n_inst; k += gridDim.x) {
@@ -62,6 +66,16 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
     in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
     solve_one<N>(a, k, base, M, in, sm, a.L);
   }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallArgs a) {
+  solve_batch<N>(a);
+}
+
+template <int N>
+__global__ void __launch_bounds__(1024, 1) solve_wide_kernel(SmallArgs a) {
+  solve_batch<N>(a);
 }
 
 // fixed_batch_schedule (offline_solvers.hpp:208-214): one CTA per instance.
@@ -164,13 +178,12 @@ static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, 
   SmallArgs a = a_in;
   a.L = make_layout(a.M, N, W);
   const int smem = a.L.total;
-  cudaError_t e = cudaFuncSetAttribute(solve_small_kernel<N>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = threads > 256 ? solve_wide_kernel<N> : solve_small_kernel<N>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(solve_small_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           100);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  solve_small_kernel<N><<<grid, threads, smem, st>>>(a);
+  kern<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
