@@ -1,5 +1,5 @@
 """C5 (BASELINE.json configs[4]): online episodes, TW(0, OG), 10^5 slots.
-usage: python scripts/bench_online.py [episodes] [horizon] [heavy|light]"""
+usage: python scripts/bench_online.py [episodes] [horizon] [heavy|light] [tw|local]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -12,7 +12,8 @@ M = 14
 prof = profile_heavy(M) if kind == "heavy" else profile_light(M)
 lo, hi, p = (0.25, 1.0, 0.05) if kind == "heavy" else (0.05, 0.2, 0.25)
 users = sample_batch(1, M, prof, hi, hi, seed=7)  # the CLI: sample_scenario(users, fixed(l_high))
-cfg = OnlineConfig("bernoulli", p, lo, hi, 0.025, "og", "tw", 0, None, H)
+policy = sys.argv[4] if len(sys.argv) > 4 else "tw"
+cfg = OnlineConfig("bernoulli", p, lo, hi, 0.025, "og", policy, 0, None, H)
 eng = Engine(0)
 dev = {k: torch.as_tensor(v, device="cuda") for k, v in users.items()}
 seeds = torch.arange(1, E + 1, dtype=torch.int64, device="cuda")

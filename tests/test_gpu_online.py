@@ -81,3 +81,55 @@ def test_contract_errors(engine):
         engine.online(prof, users, OnlineConfig(**{**c["cfg"], "slot": 0.0}), [1])
     with pytest.raises(ValueError):
         engine.online(prof, users, OnlineConfig(**{**c["cfg"], "p_arrive": 1.5}), [1])
+
+
+# Configurations for the warp-parallel slot loop (users on lanes, the random
+# stream split by prefix sums) against the lane-0 slot loop it replaces for
+# M <= 32, which the golden episodes pin to the reference.
+_SWEEP = [
+    ("heavy", 14, dict(arrival="bernoulli", p_arrive=0.05, l_low=0.25, l_high=1.0, solver="og", policy="tw", window=0)),
+    ("light", 14, dict(arrival="bernoulli", p_arrive=0.25, l_low=0.05, l_high=0.2, solver="og", policy="tw", window=0)),
+    ("heavy", 32, dict(arrival="bernoulli", p_arrive=0.3, l_low=0.25, l_high=1.0, solver="og", policy="tw", window=2)),
+    ("heavy", 1, dict(arrival="bernoulli", p_arrive=0.5, l_low=0.25, l_high=1.0, solver="og", policy="tw", window=0)),
+    ("heavy", 9, dict(arrival="immediate", p_arrive=0.0, l_low=0.25, l_high=1.0, solver="ipssa", policy="tw", window=1)),
+    ("heavy", 12, dict(arrival="bernoulli", p_arrive=1.0, l_low=0.4, l_high=0.4, solver="og", policy="tw", window=3)),
+    ("light", 20, dict(arrival="bernoulli", p_arrive=0.6, l_low=0.05, l_high=0.2, solver="ipssa", policy="local", window=0)),
+    ("heavy", 7, dict(arrival="bernoulli", p_arrive=0.0, l_low=0.25, l_high=1.0, solver="og", policy="tw", window=0)),
+]
+
+
+def _sweep_runs(engine, horizon, episodes):
+    from paper_2206_06304_b200 import profile_heavy, profile_light, sample_batch
+    res = []
+    for kind, M, kw in _SWEEP:
+        prof = profile_heavy(M) if kind == "heavy" else profile_light(M)
+        hi = kw["l_high"]
+        users = sample_batch(1, M, prof, hi, hi, seed=M)
+        cfg = OnlineConfig(slot=0.025, horizon=horizon, **kw)
+        out = engine.online(prof, users, cfg, list(range(1, episodes + 1)), n_trace=2)
+        res.append({k: np.asarray(v) for k, v in out.items()})
+    return res
+
+
+def test_warp_slot_loop_matches_serial_loop(engine, tmp_path):
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, pickle
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import test_gpu_online as t
+from paper_2206_06304_b200 import Engine
+pickle.dump(t._sweep_runs(Engine(0), 4000, 24), open(sys.argv[1], "wb"))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp_path / "serial.pkl")
+    r = subprocess.run([sys.executable, "-c", code, path], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, COINFER_ONLINE_SERIAL="1"), timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    import pickle
+    serial = pickle.load(open(path, "rb"))
+    warp = _sweep_runs(engine, 4000, 24)
+    for (kind, M, kw), a, b in zip(_SWEEP, warp, serial):
+        for k in a:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=f"{kind} M={M} {kw} {k}")
+        assert (a["status"] == 0).all(), (kind, M, kw)
