@@ -666,6 +666,17 @@ __global__ void __launch_bounds__(32) online_warp_kernel(OnlineArgs o) {
   }
 }
 
+#ifdef CFB_PHASE_TIMING
+extern "C" int coinfer_debug_online_phase_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
 int online_warp_smem_bytes(int M, int N) {
   const int solver = make_layout(M, N, 1).total;
   return solver + 8 * 7 * M + 8 * 312 + 8 * 128 + 4 * 32 + 16;
