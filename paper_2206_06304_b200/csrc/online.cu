@@ -388,7 +388,10 @@ __device__ __forceinline__ double lane_fold(double acc, double v, unsigned take,
 }  // namespace
 
 template <int N>
-__global__ void __launch_bounds__(32) online_warp_kernel(OnlineArgs o) {
+#ifndef CFB_ONLINE_WARP_MINB
+#define CFB_ONLINE_WARP_MINB 16  // 128 registers: 16 episodes per SM (measured best of 1/16/21/32)
+#endif
+__global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(OnlineArgs o) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int M = o.M;  // <= 32
   const int lane = threadIdx.x;
