@@ -1,12 +1,14 @@
-"""Per-phase SM cycles of the fused kernel (needs a -DCFB_PHASE_TIMING build via COINFER_LIB)."""
+"""Per-phase SM cycles of the fused kernel (needs a -DCFB_PHASE_TIMING build via COINFER_LIB):
+python scripts/phase_time.py [instances] [M]"""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2206_06304_b200 import Engine, profile_heavy, sample_batch, _abi
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+M = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 eng = Engine(0)
-prof = profile_heavy(50)
-dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, 50, prof, seed=1).items()}
+prof = profile_heavy(M)
+dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, M, prof, seed=1).items()}
 eng.sweep(prof, dev); torch.cuda.synchronize()
 buf = (C.c_ulonglong * 10)()
 lib = _abi.load_library()
