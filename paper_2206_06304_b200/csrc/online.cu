@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
         in.has_l_ip = false;  // IP-SSA at min deadline, as invoke_solver does
         in.l_ip = 0.0;
         const Layout L = make_layout(ns, N, 1);
-        solve_one<N>(o.solve, e, obase, ns, in, sm, L);
+        solve_one<N, true>(o.solve, e, obase, ns, in, sm, L);
         __syncthreads();
         if (tid == 0) {
           const int ns2 = ivars[3];
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
         in.has_l_ip = false;  // IP-SSA at min deadline, as invoke_solver does
         in.l_ip = 0.0;
         const Layout L = make_layout(ns, N, 1);
-        solve_one<N>(o.solve, e, obase, ns, in, sm, L);
+        solve_one<N, true>(o.solve, e, obase, ns, in, sm, L);
         __syncthreads();
         const bool og = o.solve.do_og;
         const int stt = og ? o.solve.og.status[e] : o.solve.ip.status[e];
