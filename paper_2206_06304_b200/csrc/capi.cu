@@ -237,6 +237,12 @@ void patch_og_out(unsigned char* b, coinfer_og_out& o) {
   patch(b, o.group_batch_size);
 }
 
+#ifndef CFB_E2E_CHUNKS
+#define CFB_E2E_CHUNKS 32  // host-memory batches: up to this many chunks pipelined over two streams
+#endif
+#ifndef CFB_E2E_MINCHUNK
+#define CFB_E2E_MINCHUNK 32768  // instances per chunk, at least (measured: 8 / 16 / 32 chunks of 1M: 8.17 / 8.40 / 8.53M/s e2e)
+#endif
 constexpr int kSmallMaxM = 255;  // u8 group/bound indices in shared memory
 
 // Instances too large for one CTA's shared memory: the multi-kernel path of
@@ -441,7 +447,7 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
 
   // Host memory: chunk the batch and alternate two streams, so the H2D copy
   // of chunk c+1 and the D2H copy of chunk c-1 overlap the solve of chunk c.
-  const size_t nch = K >= 131072 ? (K / 65536 < 8 ? K / 65536 : 8) : 1;
+  const size_t nch = K >= 131072 ? (K / CFB_E2E_MINCHUNK < CFB_E2E_CHUNKS ? K / CFB_E2E_MINCHUNK : CFB_E2E_CHUNKS) : 1;
   for (size_t c = 0; c < nch; ++c) {
     const size_t k0 = K * c / nch, k1 = K * (c + 1) / nch, Kc = k1 - k0;
     const int slot = (int)(c & 1);
