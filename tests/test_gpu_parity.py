@@ -180,6 +180,20 @@ def test_device_and_host_paths_agree(engine):
     ck.assert_same_og(og_h, og_d)
 
 
+def test_host_pipeline_chunks_agree_with_device(engine):
+    """Host batches of >= 131072 instances go through the chunked two-stream
+    pipeline (up to 32 chunks); their results must equal one device launch."""
+    import torch
+    prof = profile_heavy(12)
+    users = sample_batch(140_000, 12, prof, 0.25, 1.0, seed=13)
+    ip_h, og_h = engine.sweep(prof, users)
+    dev = {k: torch.as_tensor(v, device="cuda") for k, v in users.items()}
+    ip_d, og_d = engine.sweep(prof, dev)
+    engine.synchronize()
+    ck.assert_same_ip(ip_h, ip_d)
+    ck.assert_same_og(og_h, og_d)
+
+
 def test_full_size_properties(engine):
     """At large batch sizes: shard invariance, internal consistency, and a
     sampled oracle check (size-independent properties)."""
