@@ -352,9 +352,18 @@ int oracle_fixed_batch(const coinfer_profile* p, const coinfer_users* u, const d
 /* G row i by the shared left fold: for a fixed group
    start i and assumed bound b, the per-user choices do not depend on the
    group end j, and total_energy is a prefix-consistent left fold, so the
-   energies of all groups i..j come out of one pass over j.  Bit-identical
-   to calling try_ip_ssa(subscenario(i..j), dl[i]) per cell (verified in
-   tests against the direct form below and against the reference). */
+   energies of all groups i..j come out of one pass over j.  Two exact cuts
+   (SURVEY §7 "b-pruning"):
+     * every bound b >= b0 (the first whose pipeline does not fit dl[i];
+       feasibility is monotone in b) sends every user local-only
+       (try_fixed_batch:148-150) with the same energies, so those bounds
+       collapse into one pass keyed with the largest admissible bound,
+       b = j-i+1 (the reference's descending-b scan with strict '<' keeps
+       the largest b among equal energies);
+     * a chain whose offloader count exceeds b is never admissible again
+       (the count never decreases along j), so it stops there.
+   Bit-identical to calling try_ip_ssa(subscenario(i..j), dl[i]) per cell
+   (tests compare the two forms cell by cell and against the reference). */
 static void g_row_fast(const inst_t* s, const int* order, int i, double* G, int* B) {
   const int M = s->M, N = s->N;
   const double dli = s->dl[order[i]];
@@ -362,23 +371,46 @@ static void g_row_fast(const inst_t* s, const int* order, int i, double* G, int*
     G[j] = INFINITY;
     B[j] = 0;
   }
-  for (int b = 1; b <= M - i; ++b) {
+  int b0 = 1;  /* first bound whose pipeline does not fit dl[i] (or M-i+1) */
+  {
+    int lo = 1, hi = M - i + 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) / 2;
+      double st[COINFER_MAX_SUBTASKS];
+      if (batch_start_times(s, dli, mid, st)) lo = mid + 1; else hi = mid;
+    }
+    b0 = lo;
+  }
+  for (int b = 1; b < b0; ++b) {
     double st[COINFER_MAX_SUBTASKS];
-    const int feas = batch_start_times(s, dli, b, st);
+    batch_start_times(s, dli, b, st);
     double total = 0.0;
     int offl = 0;
     for (int j = i; j < M; ++j) {
       const int m = order[j];
-      const choice_t c = feas ? best_partition(s, m, st, s->dl[m]) : local_only_choice(s, m, s->dl[m]);
+      const choice_t c = best_partition(s, m, st, s->dl[m]);
       if (!c.feasible) break;
       const double f = sched_freq(s, m, &c);
       total = fold_user(s, m, c.split, f, total);
       offl += c.split < N;
-      if (b <= j - i + 1 && offl <= b) {
-        if (total < G[j] || (total == G[j] && b > B[j])) {
-          G[j] = total;
-          B[j] = b;
-        }
+      if (offl > b) break;
+      if (b <= j - i + 1 && (total < G[j] || (total == G[j] && b > B[j]))) {
+        G[j] = total;
+        B[j] = b;
+      }
+    }
+  }
+  if (b0 <= M - i) { /* the all-local pass: bounds b0..j-i+1 */
+    double total = 0.0;
+    for (int j = i; j < M; ++j) {
+      const int m = order[j];
+      const choice_t c = local_only_choice(s, m, s->dl[m]);
+      if (!c.feasible) break;
+      total = fold_user(s, m, N, c.freq, total);
+      const int b = j - i + 1;
+      if (b >= b0 && (total < G[j] || (total == G[j] && b > B[j]))) {
+        G[j] = total;
+        B[j] = b;
       }
     }
   }
@@ -447,36 +479,50 @@ static int og_one(const inst_t* s, int fast, int64_t k, coinfer_og_out* out) {
     }
   }
 
-  /* DP (offline_solvers.hpp:313-330) */
+  /* DP (offline_solvers.hpp:313-330).  S is stored transposed (column i-1
+     is contiguous: the prev loop reads it in order) and sum_latency(size)
+     is tabulated once; the comparisons and their order are the reference's. */
+  double* sl = malloc(sizeof(double) * (M + 1));
+  for (int z = 1; z <= M; ++z) sl[z] = sum_latency(s, z);
   for (size_t x = 0; x < MM; ++x) {
     S[x] = INFINITY;
     parent[x] = -1;
   }
-  for (int j = 0; j < M; ++j) S[j] = G[j];
-  for (int i = 1; i < M; ++i)
+#define ST(row, col) S[(size_t)(col) * M + (row)]
+  for (int j = 0; j < M; ++j) ST(0, j) = G[j];
+  for (int i = 1; i < M; ++i) {
+    const double* col = &ST(0, i - 1);
     for (int j = i; j < M; ++j) {
       const double g = G[(size_t)i * M + j];
       if (g == INFINITY) continue;
-      const int size = j - i + 1;
+      const double thr = sl[j - i + 1];
+      double best = INFINITY;
+      int bp = -1;
       for (int prev = 0; prev < i; ++prev) {
-        const double sp_ = S[(size_t)prev * M + i - 1];
+        const double sp_ = col[prev];
         if (sp_ == INFINITY) continue;
-        if (!(dl[prev] + sum_latency(s, size) <= dl[i])) continue;
+        if (!(dl[prev] + thr <= dl[i])) continue;  /* groups_fit */
         const double cand = sp_ + g;
-        if (cand < S[(size_t)i * M + j]) {
-          S[(size_t)i * M + j] = cand;
-          parent[(size_t)i * M + j] = prev;
+        if (cand < best) {
+          best = cand;
+          bp = prev;
         }
       }
+      ST(i, j) = best;
+      parent[(size_t)i * M + j] = bp;
     }
+  }
   int best_i = 0;
   for (int i = 1; i < M; ++i)
-    if (S[(size_t)i * M + M - 1] < S[(size_t)best_i * M + M - 1]) best_i = i;
+    if (ST(i, M - 1) < ST(best_i, M - 1)) best_i = i;
+  const double s_best = ST(best_i, M - 1);
+#undef ST
+  free(sl);
 
   if (out->order)
     for (int i = 0; i < M; ++i) out->order[(size_t)k * M + i] = order[i];
 
-  if (S[(size_t)best_i * M + M - 1] == INFINITY) {
+  if (s_best == INFINITY) {
     /* lc_solve fallback (offline_solvers.hpp:336-348, 255-276) */
     double total = 0.0;
     for (int m = 0; m < M; ++m) {

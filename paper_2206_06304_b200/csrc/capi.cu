@@ -394,6 +394,10 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   if (large && mode != Mode::Fixed) {
     // one instance at a time through solve_large.cu; host batches are staged whole
     if (users->mem == COINFER_MEM_DEVICE) return run_large_device(ctx, a, ctx->stream);
+    // the large workspace (ctx->big) is shared with device-memory calls on
+    // ctx->stream, which may still be running: order this call after them
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "synchronize before large host call");
     Stager st{ctx};
     plan_in(st, a.fmin, K * M);
     plan_in(st, a.fmax, K * M);
@@ -447,7 +451,8 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
 
   // Host memory: chunk the batch and alternate two streams, so the H2D copy
   // of chunk c+1 and the D2H copy of chunk c-1 overlap the solve of chunk c.
-  const size_t nch = K >= 131072 ? (K / CFB_E2E_MINCHUNK < CFB_E2E_CHUNKS ? K / CFB_E2E_MINCHUNK : CFB_E2E_CHUNKS) : 1;
+  size_t nch = K / CFB_E2E_MINCHUNK < CFB_E2E_CHUNKS ? K / CFB_E2E_MINCHUNK : CFB_E2E_CHUNKS;
+  if (K < 4 * (size_t)CFB_E2E_MINCHUNK || nch < 1) nch = 1;  // small batches: one chunk
   for (size_t c = 0; c < nch; ++c) {
     const size_t k0 = K * c / nch, k1 = K * (c + 1) / nch, Kc = k1 - k0;
     const int slot = (int)(c & 1);

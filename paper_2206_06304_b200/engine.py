@@ -75,11 +75,12 @@ def _kind(ctype) -> str:
 _PINNED = {}
 
 
-def _pinned_buffer(name, shape, dtype):
+def _pinned_buffer(owner, name, shape, dtype):
     """Reusable page-locked staging array (allocating pinned memory per call
     costs more than the copy).  Results in it are overwritten by the next
-    pinned call with the same output."""
-    key = (name, tuple(shape), np.dtype(dtype).str)
+    pinned call with the same output.  `owner` (the output struct) is part of
+    the key: IP-SSA and OG share field names (status, energy, split, ...)."""
+    key = (owner, name, tuple(shape), np.dtype(dtype).str)
     a = _PINNED.get(key)
     if a is None:
         a = torch.empty(shape, dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True).numpy()
@@ -132,7 +133,7 @@ class Packed:
             if mem == _abi.MEM_DEVICE:
                 a = torch.empty(shapes[dim], dtype=getattr(torch, _TT[k]), device=device)
             elif self.pinned:  # page-locked host outputs: D2H at full PCIe speed
-                a = _pinned_buffer(name, shapes[dim], _NP[k])
+                a = _pinned_buffer(struct.__name__, name, shapes[dim], _NP[k])
             else:
                 a = np.zeros(shapes[dim], dtype=_NP[k])
             arrays[name] = a

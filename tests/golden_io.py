@@ -34,3 +34,22 @@ def load(name):
 
 def all_cases():
     return load("kat") + load("random") + load("cli")
+
+
+def load_large():
+    """tests/golden/large.npz (made by tests/golden/make_large.py): name ->
+    dict(profile, users, og, ip) with exact bits."""
+    z = np.load(os.path.join(GOLDEN, "large.npz"))
+    out = {}
+    for key in z.files:
+        name, rest = key.split("/", 1)
+        d = out.setdefault(name, dict(users={}, og={}, ip={}, p={}))
+        if rest.startswith(("users/", "og/", "ip/")):
+            kind, field = rest.split("/", 1)
+            d[kind][field] = z[key]
+        else:
+            d["p"][rest] = z[key]
+    for d in out.values():
+        p = d.pop("p")
+        d["profile"] = ProfileArrays(p["work"], p["data_bits"], p["latency"])
+    return out

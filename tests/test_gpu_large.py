@@ -83,8 +83,10 @@ print("forced-large ok", n)
 
 
 def test_c4_shape_properties(engine):
-    """M = 4096 (config 4): runs, the plan is internally consistent, and the
-    group count / energies agree with the O(M^3 N) oracle form on a sub-instance."""
+    """M = 4096 (config 4) on a second instance stream: runs, and the plan is
+    internally consistent (energy = left fold of the group energies, groups
+    cover the users in deadline order).  Bit-exact C4 parity against the
+    O(M^3 N) oracle is tests/test_large_golden.py."""
     M = 4096
     prof = profile_heavy(M)
     users = sample_batch(1, M, prof, 0.25, 1.0, seed=4)

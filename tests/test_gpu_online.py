@@ -133,3 +133,37 @@ pickle.dump(t._sweep_runs(Engine(0), 4000, 24), open(sys.argv[1], "wb"))
         for k in a:
             np.testing.assert_array_equal(a[k], b[k], err_msg=f"{kind} M={M} {kw} {k}")
         assert (a["status"] == 0).all(), (kind, M, kw)
+
+
+C5 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "online_c5.json")))
+
+
+@pytest.mark.parametrize("c", C5, ids=[c["name"] for c in C5])
+def test_c5_full_horizon_episode(engine, c):
+    """BASELINE config 5 at its full 10^5-slot horizon (heavy and light),
+    slot for slot against the reference run_episode (tests/golden/
+    make_online_c5.py): every 1,000-slot block of the trace must hash equal,
+    and the episode totals and counts must be equal."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_online_c5 import block_digests
+    prof, users, cfg = _case(c)
+    out = engine.online(prof, users, cfg, [c["seed"]], n_trace=1)
+    assert out["status"][0] == 0
+    got = block_digests({k: out[k][0] for k in ("trace_reward", "trace_energy", "trace_pending",
+                                                 "trace_edge_busy")})
+    bad = [i for i, (x, y) in enumerate(zip(got, c["digests"])) if x != y]
+    assert not bad, f"first differing block: slots {bad[0] * c['block']}..{(bad[0] + 1) * c['block'] - 1}"
+    np.testing.assert_array_equal(out["totals"][0], np.array(c["totals"]))
+    np.testing.assert_array_equal(out["counts"][0], np.array(c["counts"]))
+
+
+def test_c5_batch_matches_single_episodes(engine):
+    """Episodes batched together (one warp each) equal the same episodes run
+    alone: the golden C5 seeds inside a batch of 64."""
+    c = C5[0]
+    prof, users, cfg = _case(c)
+    seeds = [c["seed"]] + [c["seed"] + 1 + e for e in range(63)]
+    out = engine.online(prof, users, cfg, seeds)
+    np.testing.assert_array_equal(out["totals"][0], np.array(c["totals"]))
+    np.testing.assert_array_equal(out["counts"][0], np.array(c["counts"]))

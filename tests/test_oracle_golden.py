@@ -126,3 +126,33 @@ def test_og_fast_equals_direct_gtable():
         np.testing.assert_array_equal(G, G0)
         fin = np.isfinite(G0)
         np.testing.assert_array_equal(B[fin], B0[fin])
+
+
+def test_og_fast_b_collapse_equals_direct_gtable():
+    """Rows whose pipeline stops fitting inside the row (b0 <= M - i) take the
+    collapsed all-local pass and the dead-chain cut of the fast form; it must
+    still equal per-cell try_ip_ssa bit for bit (M = 60, tight deadlines)."""
+    import ctypes as C
+    from paper_2206_06304_b200 import profile_heavy, sample_batch
+    from paper_2206_06304_b200.engine import Packed
+    M = 60
+    prof = profile_heavy(M)
+    users = sample_batch(2, M, prof, 0.25, 0.6, seed=77)
+    pk = Packed(prof, users, 0, False, False)
+    for k in range(2):
+        out = {}
+        for fast in (0, 1):
+            G = np.zeros((M, M))
+            B = np.zeros((M, M), dtype=np.int32)
+            ck.oracle().oracle_og_gtable(C.byref(pk.profile), C.byref(pk.users), k, fast,
+                                         G.ctypes.data_as(C.POINTER(C.c_double)),
+                                         B.ctypes.data_as(C.POINTER(C.c_int32)))
+            out[fast] = (G, B)
+        (G0, B0), (G1, B1) = out[0], out[1]
+        np.testing.assert_array_equal(G1, G0)
+        fin = np.isfinite(G0)
+        assert fin.sum() > M  # finite groups beyond the diagonal
+        np.testing.assert_array_equal(B1[fin], B0[fin])
+        assert (B0[fin] > 20).any()  # collapsed bounds (b >= b0 ~ 20 at l = 0.25) won cells
+    ck.assert_same_og(ck.oracle_og(prof, users, fast=True), ck.oracle_og(prof, users, fast=False),
+                      where="fast vs direct og")

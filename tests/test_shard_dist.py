@@ -4,8 +4,9 @@ Covers what bench.py does across ranks, minus the CUDA solve: each rank
 builds its own weak-scaling shard of the global instance stream, the shards
 concatenate to the single-process stream (shard invariance of the inputs),
 per-rank summary statistics (computed here by the C oracle, standing in for
-the GPU results) all-reduce to the single-process summary, and the job time
-is the max over ranks."""
+the GPU results) all-reduce to the single-process summary -- the per-instance
+decision hashes' sum and XOR bit for bit -- and the job time is the max over
+ranks."""
 import os
 import socket
 
@@ -39,8 +40,8 @@ def _worker(rank, world, port, out):
         lo, hi = shard_range(PER_RANK, rank, world)
         users = make_instances(prof, M, lo, hi, seed=3)
         ip, og = ck.oracle_ipssa(prof, users), ck.oracle_og(prof, users)
-        local = summary_stats(np, ip, og)
-        summ = reduce_summary(torch.as_tensor(local), dist)
+        stats, hashes = summary_stats(np, ip, og)
+        summ = reduce_summary((torch.as_tensor(stats), torch.as_tensor(hashes)), dist)
         slow = max_over_ranks(1.0 + rank, dist)
         out[rank] = (lo, hi, users["deadline"].copy(), summ, slow)
     finally:
@@ -81,6 +82,8 @@ def test_world2_gloo_sweep_reduction():
         assert (lo, hi) == (PER_RANK * r, PER_RANK * (r + 1))
         assert slow == float(world)  # max over ranks
         for k, v in expect.items():
-            # energies: a sum of two partial sums vs one sum -> allow rounding
-            assert summ[k] == pytest.approx(v, rel=1e-12), k
+            if k.startswith("decision_hash"):  # decisions: exact, whatever the sharding
+                assert summ[k] == v, k
+            else:  # energies: a sum of two partial sums vs one sum -> allow rounding
+                assert summ[k] == pytest.approx(v, rel=1e-12), k
     assert expect["failed_instances"] == 0
