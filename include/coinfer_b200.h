@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define COINFER_ABI_VERSION 2
+#define COINFER_ABI_VERSION 3
 
 /* Call-level return codes. */
 #define COINFER_OK 0
@@ -212,6 +212,12 @@ typedef struct coinfer_online_out {
   double* trace_energy;      /* [n_trace*horizon] */
   int32_t* trace_pending;    /* [n_trace*horizon] */
   double* trace_edge_busy;   /* [n_trace*horizon] */
+  /* optional (NULL: not written) */
+  int32_t* trace_action;     /* [n_trace*horizon] TraceRow::action_c, the policy's mode */
+  int32_t* trace_forced;     /* [n_trace*horizon] TraceRow::forced_count */
+  double* final_state;       /* [n_ep*(2*M+1)] OnlineEnv state after the last slot:
+                                MdpState::deadline[M], expiry_[M], MdpState::edge_busy */
+  int64_t* draws;            /* [n_ep] mt19937_64 outputs consumed (rng_ = seed, discard(draws)) */
 } coinfer_online_out;
 
 int coinfer_abi_version(void);

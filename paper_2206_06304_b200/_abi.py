@@ -15,7 +15,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("COINFER_LIB") or os.path.join(_HERE, "libcoinfer_b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 OK, E_ARG, E_PROFILE, E_CUDA, E_UNSUPPORTED = 0, 1, 2, 3, 4
 ST_OK, ST_INFEASIBLE = 0, 1
 ST_BAD_FREQ, ST_NEG_KAPPA, ST_BAD_RATE, ST_NEG_POWER = 10, 11, 12, 13
@@ -111,7 +111,8 @@ class OnlineCfg(C.Structure):
 class OnlineOut(C.Structure):
     _fields_ = [("status", _i32p), ("totals", _dp), ("counts", _i64p), ("n_trace", C.c_int64),
                 ("trace_reward", _dp), ("trace_energy", _dp), ("trace_pending", _i32p),
-                ("trace_edge_busy", _dp)]
+                ("trace_edge_busy", _dp), ("trace_action", _i32p), ("trace_forced", _i32p),
+                ("final_state", _dp), ("draws", _i64p)]
 
 
 # name -> (restype, argtypes) of every symbol include/coinfer_b200.h declares

@@ -978,6 +978,10 @@ int coinfer_online_run(coinfer_ctx* ctx, const coinfer_profile* profile,
   a.tr_energy = out->trace_energy;
   a.tr_pending = out->trace_pending;
   a.tr_busy = out->trace_edge_busy;
+  a.tr_action = out->trace_action;
+  a.tr_forced = out->trace_forced;
+  a.fin_state = out->final_state;
+  a.draws = reinterpret_cast<long long*>(out->draws);
 
   const bool host = sc->mem == COINFER_MEM_HOST;
   Stager st{ctx};
@@ -999,6 +1003,10 @@ int coinfer_online_run(coinfer_ctx* ctx, const coinfer_profile* profile,
     plan_out(st, a.tr_energy, T);
     plan_out(st, a.tr_pending, T);
     plan_out(st, a.tr_busy, T);
+    plan_out(st, a.tr_action, T);
+    plan_out(st, a.tr_forced, T);
+    plan_out(st, a.fin_state, E * (2 * M + 1));
+    plan_out(st, a.draws, E);
   }
   // per-episode solver scratch, device only
   int32_t* s_status = reinterpret_cast<int32_t*>(st.reserve(4 * E) + 1);
@@ -1029,6 +1037,10 @@ int coinfer_online_run(coinfer_ctx* ctx, const coinfer_profile* profile,
     patch(b, a.tr_energy);
     patch(b, a.tr_pending);
     patch(b, a.tr_busy);
+    patch(b, a.tr_action);
+    patch(b, a.tr_forced);
+    patch(b, a.fin_state);
+    patch(b, a.draws);
     for (const auto& x : st.in) {
       e = cudaMemcpyAsync(b + x.off, x.host, x.bytes, cudaMemcpyHostToDevice, sp);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D online inputs");

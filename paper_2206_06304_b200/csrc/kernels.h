@@ -58,6 +58,9 @@ struct OnlineArgs {
   int64_t n_trace;
   double *tr_reward, *tr_energy, *tr_busy;
   int32_t* tr_pending;
+  int32_t *tr_action, *tr_forced;  // optional
+  double* fin_state;               // optional: [n_ep][2M+1] deadline, expiry, edge_busy
+  long long* draws;                // optional: [n_ep] rng outputs consumed
 };
 
 // Arguments of the large-instance path (solve_large.cu); one instance per

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
     long long n_forced = 0, n_calls = 0, n_tasks = 0, n_groups = 0, n_batches = 0, n_batched = 0;
     const bool trace = e < o.n_trace;
     const size_t tbase = (size_t)e * (size_t)o.horizon;
+    long long ndraw = 0;  // mt19937_64 outputs consumed
 
     // sample_arrivals (online_sim.hpp:235-249), lane 0
     auto sample_arrivals = [&]() {
@@ -134,8 +135,12 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
         if (!(now > expiry[m])) continue;
         if (!o.immediate) {
           if (o.p_arrive <= 0.0) continue;
-          if (o.p_arrive < 1.0 && rng.uniform(0.0, 1.0) >= o.p_arrive) continue;
+          if (o.p_arrive < 1.0) {
+            ++ndraw;
+            if (rng.uniform(0.0, 1.0) >= o.p_arrive) continue;
+          }
         }
+        ndraw += o.l_low < o.l_high;
         const double l = o.l_low < o.l_high ? rng.uniform(o.l_low, o.l_high) : o.l_low;
         lrem[m] = l;
         expiry[m] = __dadd_rn(now, l);
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
 
     for (long long t = 0; t < o.horizon; ++t) {
       double energy = 0.0, forced = 0.0, busy_before = 0.0;
-      int pending_before = 0;
+      int pending_before = 0, pmode = 0;
       long long f_count = 0;
       // ------------------------------------------- policy + step (lane 0)
       if (tid == 0) {
@@ -169,6 +174,7 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
         } else {
           ++wait;
         }
+        pmode = mode;  // TraceRow::action_c: the policy's action, before step() clamps it
         const double l_th = smin(smax(th, 0.0), o.l_high);
         if (mode == 2 && ebusy > 0.0) mode = 0;
         ivars[1] = 0;
@@ -288,6 +294,8 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
           if (o.tr_energy) o.tr_energy[tbase + t] = energy;
           if (o.tr_pending) o.tr_pending[tbase + t] = pending_before;
           if (o.tr_busy) o.tr_busy[tbase + t] = busy_before;
+          if (o.tr_action) o.tr_action[tbase + t] = pmode;
+          if (o.tr_forced) o.tr_forced[tbase + t] = (int32_t)f_count;
         }
       }
       __syncthreads();
@@ -295,6 +303,15 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
     }
     if (tid == 0) {
       if (o.status) o.status[e] = ivars[2];
+      if (o.draws) o.draws[e] = ndraw;
+      if (o.fin_state) {
+        double* fs = o.fin_state + (size_t)e * (2 * M + 1);
+        for (int m = 0; m < M; ++m) {
+          fs[m] = lrem[m];
+          fs[M + m] = expiry[m];
+        }
+        fs[2 * M] = ebusy;
+      }
       if (o.totals) {
         o.totals[(size_t)e * 3 + 0] = tot_energy;
         o.totals[(size_t)e * 3 + 1] = tot_forced;
@@ -469,7 +486,7 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
       __syncwarp();
     };
     double lrem = 0.0, expiry = -1.0;
-    long long tick = 0;
+    long long tick = 0, ndraw = 0;  // ndraw: mt19937_64 outputs consumed
     const bool imm = o.immediate != 0;
     const bool coin = !imm && o.p_arrive > 0.0 && o.p_arrive < 1.0;  // a Bernoulli draw per eligible user
     const bool never = !imm && !(o.p_arrive > 0.0);
@@ -510,6 +527,7 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
           }
           wbeg += total;
           wcnt -= total;
+          ndraw += total;
           return;
         }
       }
@@ -541,8 +559,10 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
       } else {
         ++wait;
       }
+      const int pmode = mode;  // TraceRow::action_c: the policy's action, before step() clamps it
       const double l_th = smin(smax(th, 0.0), o.l_high);
       if (mode == 2 && ebusy > 0.0) mode = 0;
+      int n_resc = 0;
       if (mode == 1) {  // process_all_local (online_sim.hpp:182-191), user order
         double term = 0.0;
         if ((pend >> lane) & 1u) {
@@ -626,7 +646,8 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
         if (rm) {
           const double term = resc ? __dmul_rn(__dmul_rn(__dmul_rn(ukap, W), ufmax), ufmax) : 0.0;
           forced = lane_fold(forced, term, rm, M);
-          n_forced += __popc(rm);
+          n_resc = __popc(rm);
+          n_forced += n_resc;
           if (resc) lrem = 0.0;
         }
       }
@@ -644,12 +665,21 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
         if (o.tr_energy) o.tr_energy[tbase + t] = energy;
         if (o.tr_pending) o.tr_pending[tbase + t] = pending_before;
         if (o.tr_busy) o.tr_busy[tbase + t] = busy_before;
+        if (o.tr_action) o.tr_action[tbase + t] = pmode;
+        if (o.tr_forced) o.tr_forced[tbase + t] = n_resc;
       }
       if (status != COINFER_ST_OK) break;
     }
     (void)users;
+    if (o.fin_state && own) {
+      double* fs = o.fin_state + (size_t)e * (2 * M + 1);
+      fs[lane] = lrem;
+      fs[M + lane] = expiry;
+      if (lane == 0) fs[2 * M] = ebusy;
+    }
     if (lane == 0) {
       if (o.status) o.status[e] = status;
+      if (o.draws) o.draws[e] = ndraw;
       if (o.totals) {
         o.totals[(size_t)e * 3 + 0] = tot_energy;
         o.totals[(size_t)e * 3 + 1] = tot_forced;

@@ -442,12 +442,15 @@ class OnlineConfig:
             int(self.horizon))
 
 
-def _online(self, profile, scenarios: Dict, cfg: OnlineConfig, seeds, n_trace: int = 0):
+def _online(self, profile, scenarios: Dict, cfg: OnlineConfig, seeds, n_trace: int = 0,
+            final_state: bool = False):
     """run_episode for every seed (one GPU warp per episode).  Episode e runs
     scenario e % n_scenarios.  Returns status, totals [E,3] (total_energy,
     total_forced_cost, total_reward), counts [E,6] (forced_count,
     solver_calls, solver_tasks, solver_groups, batches, batched_tasks) and,
-    for the first n_trace episodes, per-slot reward/energy/pending/edge_busy."""
+    for the first n_trace episodes, per-slot reward/energy/pending/edge_busy/
+    action/forced.  final_state: also the OnlineEnv state after the last slot
+    ([E, 2M+1]: deadlines, expiries, edge_busy) and the rng outputs consumed."""
     mem = self._mem(scenarios)
     pk = Packed(profile, scenarios, mem, False, False)
     E = int(len(seeds))
@@ -470,13 +473,22 @@ def _online(self, profile, scenarios: Dict, cfg: OnlineConfig, seeds, n_trace: i
         out.update(trace_reward=alloc((n_trace, cfg.horizon), np.float64, torch.float64),
                    trace_energy=alloc((n_trace, cfg.horizon), np.float64, torch.float64),
                    trace_pending=alloc((n_trace, cfg.horizon), np.int32, torch.int32),
-                   trace_edge_busy=alloc((n_trace, cfg.horizon), np.float64, torch.float64))
+                   trace_edge_busy=alloc((n_trace, cfg.horizon), np.float64, torch.float64),
+                   trace_action=alloc((n_trace, cfg.horizon), np.int32, torch.int32),
+                   trace_forced=alloc((n_trace, cfg.horizon), np.int32, torch.int32))
+    if final_state:
+        out.update(final_state=alloc((E, 2 * pk.M + 1), np.float64, torch.float64),
+                   draws=alloc((E,), np.int64, torch.int64))
     oo = _abi.OnlineOut(_ptr(out["status"], C.c_int32), _ptr(out["totals"], C.c_double),
                         _ptr(out["counts"], C.c_int64), int(n_trace) if T else 0,
                         _ptr(out.get("trace_reward"), C.c_double),
                         _ptr(out.get("trace_energy"), C.c_double),
                         _ptr(out.get("trace_pending"), C.c_int32),
-                        _ptr(out.get("trace_edge_busy"), C.c_double))
+                        _ptr(out.get("trace_edge_busy"), C.c_double),
+                        _ptr(out.get("trace_action"), C.c_int32),
+                        _ptr(out.get("trace_forced"), C.c_int32),
+                        _ptr(out.get("final_state"), C.c_double),
+                        _ptr(out.get("draws"), C.c_int64))
     c = cfg.to_c()
     self._check(self.lib.coinfer_online_run(self.ctx, C.byref(pk.profile), C.byref(pk.users),
                                             C.byref(c), _ptr(sd, C.c_uint64), E, C.byref(oo)))

@@ -1,9 +1,17 @@
 #!/bin/bash
 # Development library: only the N=4 instantiations of the small solver
-# (fast to compile), linked into build/libdev.so; use COINFER_LIB=build/libdev.so.
+# (fast to compile), linked into build/libdev.so (or $OUT); use COINFER_LIB=build/libdev.so.
+# Extra nvcc flags via $EXTRA (e.g. EXTRA=-DCFB_PHASE_TIMING).
 set -e
 cd "$(dirname "$0")/../paper_2206_06304_b200/csrc"
-F="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false -Xcompiler -fPIC -DCFB_ONLY_N=4"
-for f in ${@:-solve_small}; do nvcc $F -c $f.cu -o /tmp/dev_$f.o; done
-mkdir -p ../../build
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../build/libdev.so /tmp/dev_capi.o /tmp/dev_solve_small.o /tmp/dev_solve_large.o /tmp/dev_online.o /tmp/dev_probe.o /tmp/dev_baselines.o /tmp/dev_generate.o /tmp/dev_oracles.o -lcudart
+OUT=${OUT:-../../build/libdev.so}
+F="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false -Xcompiler -fPIC -DCFB_ONLY_N=4 $EXTRA"
+T=/tmp/devobj_$$
+mkdir -p $T ../../build
+pids=()
+for f in capi solve_small solve_large online probe baselines generate oracles; do
+  nvcc $F -c $f.cu -o $T/$f.o & pids+=($!)
+done
+for p in "${pids[@]}"; do wait $p; done
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT $T/*.o -lcudart
+rm -rf $T

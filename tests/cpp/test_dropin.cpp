@@ -15,6 +15,8 @@
 #include <string>
 
 #include "coinfer/offline_solvers.hpp"
+#include "coinfer/online_sim.hpp"
+#include <memory>
 
 using namespace coinfer;
 using json = nlohmann::json;
@@ -289,4 +291,120 @@ TEST(Errors, ShapeAndContractMessages) {
   EXPECT_EQ(ip_ssa(empty, 0.1).split.size(), 0u);
   EXPECT_EQ(og(empty).groups.size(), 0u);
   EXPECT_EQ(baseline(empty, BaselineMode::FIFO).batch_size.size(), sc.profile.subtasks());
+}
+
+// ---------------------------------------------------------------- online_sim
+
+namespace {
+
+struct OnlineCase {
+  Scenario sc;
+  ArrivalModel am;
+  OnlineSolver solver;
+  double slot;
+  bool local;
+  std::size_t window;
+  double threshold;
+  std::size_t horizon;
+  std::uint64_t seed;
+};
+
+OnlineCase online_case(const json& c) {
+  OnlineCase o;
+  o.sc = scenario(c, 0);
+  const json& g = c["cfg"];
+  o.am.kind = g["arrival"] == "immediate" ? ArrivalModel::Kind::Immediate : ArrivalModel::Kind::Bernoulli;
+  o.am.p_arrive = g["p_arrive"];
+  o.am.l_low = g["l_low"];
+  o.am.l_high = g["l_high"];
+  o.solver = g["solver"] == "og" ? OnlineSolver::OG : OnlineSolver::IPSSA;
+  o.slot = g["slot"];
+  o.local = g["policy"] == "local";
+  o.window = g["window"].get<std::size_t>();
+  o.threshold = g["threshold"].is_null() ? o.am.l_high : g["threshold"].get<double>();
+  o.horizon = g["horizon"].get<std::size_t>();
+  o.seed = c["seed"].get<std::uint64_t>();
+  return o;
+}
+
+void expect_episode(const EpisodeMetrics& m, const json& e, const std::string& where) {
+  EXPECT_TRUE(same_bits(m.total_energy, e["totals"][0].get<double>())) << where;
+  EXPECT_TRUE(same_bits(m.total_forced_cost, e["totals"][1].get<double>())) << where;
+  EXPECT_TRUE(same_bits(m.total_reward, e["totals"][2].get<double>())) << where;
+  const std::size_t got[6] = {m.forced_count, m.solver_calls, m.solver_tasks,
+                              m.solver_groups, m.batches,     m.batched_tasks};
+  for (int i = 0; i < 6; ++i) EXPECT_EQ(got[i], e["counts"][i].get<std::size_t>()) << where << " count " << i;
+  ASSERT_EQ(m.trace.size(), e["trace_reward"].size()) << where;
+  std::size_t bad = 0;
+  for (std::size_t t = 0; t < m.trace.size(); ++t) {
+    const TraceRow& r = m.trace[t];
+    bad += r.slot != t || !same_bits(r.reward, e["trace_reward"][t].get<double>()) ||
+           !same_bits(r.energy, e["trace_energy"][t].get<double>()) ||
+           r.pending_count != e["trace_pending"][t].get<std::size_t>() ||
+           !same_bits(r.edge_busy, e["trace_edge_busy"][t].get<double>());
+  }
+  EXPECT_EQ(bad, 0u) << where << ": slots differing from the reference trace";
+}
+
+}  // namespace
+
+// run_episode with the fixed policies is ONE device episode; the same episode
+// stepped on the host (a policy the device driver does not know, so
+// OnlineEnv::step runs each slot and calls the GPU og / ip_ssa) must give the
+// same reference trace, the same trace actions, and leave the env in the same
+// state (deadlines, edge_busy, time, random stream position).
+TEST(Online, RunEpisodeDeviceAndHostStepMatchTheReference) {
+  for (const json& c : load("online")) {
+    const OnlineCase o = online_case(c);
+    const std::string where = c["name"];
+    OnlineEnv dev(o.sc, o.am, o.solver, o.slot, 1);
+    OnlineEnv host(o.sc, o.am, o.solver, o.slot, 1);
+    const PolicyFn fixed = o.local ? local_policy() : PolicyFn(TimeWindowPolicy(o.window, o.threshold));
+    const EpisodeMetrics md = run_episode(dev, fixed, o.horizon, o.seed);
+    auto inner = std::make_shared<PolicyFn>(fixed);  // opaque wrapper: forces the host slot loop
+    const EpisodeMetrics mh = run_episode(host, [inner](const MdpState& s) { return (*inner)(s); }, o.horizon, o.seed);
+    expect_episode(md, c["expect"], where + " (device episode)");
+    expect_episode(mh, c["expect"], where + " (host steps)");
+    for (std::size_t t = 0; t < md.trace.size(); ++t) {
+      ASSERT_EQ(md.trace[t].action_c, mh.trace[t].action_c) << where << " slot " << t;
+      ASSERT_TRUE(same_bits(md.trace[t].action_lth, mh.trace[t].action_lth)) << where << " slot " << t;
+      ASSERT_EQ(md.trace[t].forced_count, mh.trace[t].forced_count) << where << " slot " << t;
+    }
+    EXPECT_EQ(md.mean_batch_size(), mh.mean_batch_size()) << where;
+    // state after the episode, and after more host slots from it
+    for (int extra = 0; extra < 60; ++extra) {
+      ASSERT_TRUE(same_bits(dev.now(), host.now())) << where;
+      ASSERT_TRUE(same_bits(dev.state().edge_busy, host.state().edge_busy)) << where << " +" << extra;
+      for (std::size_t m = 0; m < o.sc.n_users(); ++m)
+        ASSERT_TRUE(same_bits(dev.state().deadline[m], host.state().deadline[m])) << where << " user " << m << " +" << extra;
+      const ActionVec a{extra % 3 == 2 ? 1 : 0, 0.0};
+      ASSERT_TRUE(same_bits(dev.step(a), host.step(a))) << where << " +" << extra;
+    }
+  }
+}
+
+TEST(Online, StepSolverCallEqualsOgOnTheClippedScenario) {
+  const json c = load("online")[0];
+  OnlineCase o = online_case(c);
+  o.am.p_arrive = 0.0;  // no arrivals: only the loaded state
+  OnlineEnv env(o.sc, o.am, OnlineSolver::OG, o.slot, 3);
+  const std::size_t M = o.sc.n_users();
+  MdpState s;
+  s.deadline.assign(M, 0.0);
+  for (std::size_t m = 0; m < M; m += 2) s.deadline[m] = 0.15 + 0.05 * double(m % 5);
+  env.load_state(s);
+  StepInfo info;
+  const double r = env.step({2, 0.25}, &info);
+  Scenario sub;
+  sub.profile = o.sc.profile;
+  for (std::size_t m = 0; m < M; ++m)
+    if (s.deadline[m] > 0.0) {
+      sub.users.push_back(o.sc.users[m]);
+      sub.deadline.push_back(s.deadline[m] >= 0.25 ? std::max(0.25, env.local_floor(m)) : s.deadline[m]);
+    }
+  const GroupingPlan plan = og(sub);
+  EXPECT_TRUE(same_bits(info.energy, plan.energy));
+  EXPECT_TRUE(same_bits(-r, plan.energy + info.forced_cost));
+  EXPECT_EQ(info.solver_groups, plan.groups.size());
+  EXPECT_EQ(info.solver_tasks, sub.users.size());
 }

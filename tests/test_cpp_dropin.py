@@ -54,3 +54,12 @@ def test_reference_offline_solvers_suite():
 @pytest.mark.gpu
 def test_dropin_suite():
     _run("test_dropin")
+
+
+@pytest.mark.gpu
+def test_reference_online_sim_suite():
+    """The reference's test_online_sim.cpp, unchanged, on include/coinfer/online_sim.hpp:
+    OnlineEnv::step on the host over the GPU og/ip_ssa, and run_episode with
+    the fixed policies as one device episode (coinfer_online_run)."""
+    out = _run("ref_test_online_sim")
+    assert "17 tests ran" in out
