@@ -45,8 +45,8 @@ UNIT = "instances/s"
 WORKLOAD = ("C3: IP-SSA (l = min deadline) + OG per instance, 1M independent instances x "
             "M=50 users per GPU (weak scaling: instance shards, no data-path collective), "
             "profile_heavy(b_max=50) N=4, deadlines U[0.25,1.0]")
-IP_E2E_FIELDS = ["status", "batch_bound", "energy", "split"]
-OG_E2E_FIELDS = ["status", "energy", "n_groups", "group_of_user", "split"]
+IP_E2E_FIELDS = ["status", "batch_bound", "energy", "split", "user_energy"]
+OG_E2E_FIELDS = ["status", "energy", "n_groups", "group_of_user", "split", "user_energy"]
 
 
 def parse():
@@ -62,6 +62,9 @@ def parse():
                     help="target CPU time of the bounded reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu counter pass")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -168,6 +171,68 @@ def pruned_work_model(prof, users, chunk=20000):
     return w
 
 
+def executed_work(prof, counts):
+    """SURVEY.md §8d per-unit fp64-pipe costs x the units the launch EXECUTED,
+    as counted by the instrumented solve (Engine.count_work): every (user,
+    chain) evaluation of the OG G rows, the IP-SSA chains and the b*
+    re-derivation (C_ub each), every all-local user step (C_loc), every
+    chain start (N: the start-time recursion), every DP cell (C_dp)."""
+    N = prof.N
+    C_ub, C_loc, C_dp = 19 * N - 13, 3 * N + 1, 4
+    return float((counts["og_chain_steps"] + counts["ip_chain_steps"] + counts["bstar_steps"]) * C_ub
+                 + counts["local_steps"] * C_loc + counts["chain_starts"] * N + counts["dp_cells"] * C_dp)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+NCU_METRICS = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
+               "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum",
+               "dram__bytes_write.sum", "smsp__inst_executed.sum"]
+
+
+def ncu_pass(args):
+    """One live ncu pass over the bench's own solve launch (this script,
+    --ncu-child: the same inputs, one launch): fp64-pipe activity, issue
+    activity and DRAM traffic of the dominant kernel.  None if ncu is
+    unavailable.  (Timings under ncu are never used as bench values.)"""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    out = f"/tmp/coinfer_ncu_{os.getpid()}.csv"
+    cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "-k", "regex:solve_small",
+           "-c", "1", "--csv", "--log-file", out, sys.executable, os.path.abspath(__file__), "--ncu-child",
+           "--n-inst", str(args.n_inst), "--M", str(args.M), "--seed", str(args.seed)]
+    try:
+        subprocess.run(cmd, capture_output=True, timeout=600, cwd=ROOT)
+        import csv
+        lines = [l for l in open(out) if not l.startswith("==")]
+        vals = {}
+        for r in csv.DictReader(lines):
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                     "ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+                     "msecond": 1.0, "s": 1e3, "second": 1e3}.get(r["Metric Unit"], 1.0)
+            vals[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * scale
+        os.unlink(out)
+        return {"kernel": "cfb::solve_small_kernel<4> (1 launch, the bench's inputs)",
+                "fp64_pipe_active_pct": vals.get(NCU_METRICS[1]),
+                "issue_active_pct": vals.get(NCU_METRICS[2]),
+                "dram_bytes": vals.get(NCU_METRICS[3], 0.0) + vals.get(NCU_METRICS[4], 0.0),
+                "warp_instructions": vals.get(NCU_METRICS[5]),
+                "gpu_time_ms_under_ncu": vals.get(NCU_METRICS[0]),
+                "command": "ncu --metrics " + ",".join(NCU_METRICS) + " --clock-control none -k regex:solve_small -c 1"}
+    except Exception as ex:  # noqa: BLE001 -- a measurement aid, never fatal
+        return {"error": str(ex)[:200]}
+
+
 # ----------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -247,6 +312,103 @@ def cpu_reference(prof, users, target_s, sample_cap=None):
                        f"{threads} threads, {t:.1f} s wall"), count, t
 
 
+# ------------------------------------------------------- other BASELINE configs
+
+def other_configs(eng, args, rank, world, allmax, barrier):
+    """The BASELINE.json configs besides the headline, timed in this run:
+    target (north_star: M=100 batched, with its roofline), C1 (IP-SSA M=10,
+    one instance), C2 (OG M=100, one instance), C4 (OG M=4096, one
+    instance), C5 (online, 10^5 slots, heavy and light, episodes sharded
+    over ranks).  Device-resident inputs, CUDA events (C1/C2 also the C-ABI
+    call on the host clock), max over ranks."""
+    import ctypes
+    import torch
+    from paper_2206_06304_b200 import _abi, profile_heavy, profile_light, sample_batch, sub_seed
+    from paper_2206_06304_b200.engine import OnlineConfig, Packed
+
+    def events(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    out = {}
+    # target: M=100 batched IP-SSA + OG (north_star), weak scaling like C3
+    M, K = 100, 100_000
+    prof = profile_heavy(M)
+    lo = rank * K
+    seeds = sub_seed(args.seed, 1, np.arange(lo, lo + K, dtype=np.uint64))
+    u, st = eng.sample(prof, M, seeds, 0.25, 1.0, device=True)
+    dev = {k: u[k] for k in ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline"]}
+    barrier()
+    ms = allmax(events(lambda: eng.sweep(prof, dev), 3))
+    counts = eng.count_work(prof, dev)
+    w = executed_work(prof, counts)
+    peak = eng.fp64_peak()
+    out["target_M100"] = {"workload": f"IP-SSA + OG, {K} instances x M=100 per GPU, profile_heavy(100), "
+                                      "deadlines U[0.25,1.0], the CLI stream", "metric": "instances/s",
+                          "value": K * world / (ms * 1e-3), "ms_per_step": ms,
+                          "roofline": {"achieved": w / (ms * 1e-3) / 1e12, "peak": peak / 1e12,
+                                       "frac": w / (ms * 1e-3) / peak, "unit": "TFLOP/s",
+                                       "executed_units": counts}}
+    del dev, u
+    # C1 / C2: one instance per call; C4: one M=4096 instance
+    for name, M, lo_, hi_, mode, reps in [("C1", 10, 0.25, 0.25, "ipssa", 200), ("C2", 100, 0.25, 1.0, "og", 100),
+                                          ("C4", 4096, 0.25, 1.0, "og", 3)]:
+        prof = profile_heavy(M)
+        dev = {k: torch.as_tensor(v, device=f"cuda:{eng.device}")
+               for k, v in sample_batch(1, M, prof, lo_, hi_, seed=7).items()}
+        pk = Packed(prof, dev, _abi.MEM_DEVICE, mode == "ipssa", mode != "ipssa", f"cuda:{eng.device}")
+        if mode == "ipssa":
+            call = lambda: eng.lib.coinfer_ipssa_batch(eng.ctx, ctypes.byref(pk.profile),  # noqa: E731
+                                                       ctypes.byref(pk.users), None, ctypes.byref(pk.out_ip))
+        else:
+            call = lambda: eng.lib.coinfer_og_batch(eng.ctx, ctypes.byref(pk.profile),  # noqa: E731
+                                                    ctypes.byref(pk.users), ctypes.byref(pk.out_og))
+        dev_ms = allmax(events(call, reps))
+        lat = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            assert call() == 0
+            eng.synchronize()
+            lat.append(time.perf_counter() - t0)
+        lat.sort()
+        out[name] = {"workload": f"{'IP-SSA' if mode == 'ipssa' else 'OG'}, one instance, M={M}, profile_heavy",
+                     "device_ms_per_solve": dev_ms, "abi_call_ms_median": allmax(lat[len(lat) // 2] * 1e3),
+                     "abi_call_ms_best": allmax(lat[0] * 1e3), "calls": reps}
+    # C5: online episodes, TW(0, OG), 10^5 slots; episodes sharded over ranks
+    E, H = 4096, 100_000
+    for kind in ["heavy", "light"]:
+        M = 14
+        prof = profile_heavy(M) if kind == "heavy" else profile_light(M)
+        lo_, hi_, p = (0.25, 1.0, 0.05) if kind == "heavy" else (0.05, 0.2, 0.25)
+        users = sample_batch(1, M, prof, hi_, hi_, seed=7)  # the CLI: sample_scenario(users, fixed(l_high))
+        dev = {k: torch.as_tensor(v, device=f"cuda:{eng.device}") for k, v in users.items()}
+        cfg = OnlineConfig("bernoulli", p, lo_, hi_, 0.025, "og", "tw", 0, None, H)
+        seeds = torch.arange(1 + rank * E, 1 + (rank + 1) * E, dtype=torch.int64, device=f"cuda:{eng.device}")
+        eng.online(prof, dev, OnlineConfig(**{**cfg.__dict__, "horizon": 100}), seeds[:256])
+        torch.cuda.synchronize()
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        res = eng.online(prof, dev, cfg, seeds)
+        e.record()
+        torch.cuda.synchronize()
+        ms = allmax(s.elapsed_time(e))
+        c = res["counts"].cpu().numpy()
+        out[f"C5_{kind}"] = {"workload": f"online TW(0, OG), M=14, {kind} (p={p}, U[{lo_},{hi_}]), "
+                                         f"{H} slots, {E} episodes per GPU",
+                             "metric": "episodes/s", "value": E * world / (ms * 1e-3), "ms": ms,
+                             "ok": bool((res["status"] == 0).all().item()),
+                             "mean_solver_calls_per_episode": float(c[:, 1].mean())}
+    return out
+
+
 # ---------------------------------------------------------------- main
 
 def main():
@@ -290,9 +452,23 @@ def main():
     from paper_2206_06304_b200 import Engine
     from paper_2206_06304_b200.shard import max_over_ranks, reduce_summary, summary_stats
 
+    if args.ncu_child:  # one solve launch of the bench's inputs, under ncu (ncu_pass)
+        eng = Engine(0)
+        prof, dev, _, _ = make_inputs(args, 0, 1, eng)
+        torch.cuda.synchronize()
+        eng.sweep(prof, dev)
+        torch.cuda.synchronize()
+        return 0
+
     torch.cuda.set_device(local)
+    nccl = None
     if world > 1:
+        # communicator set-up lines (rank, nranks, NVLS/NVLink paths) go to the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nccl = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
     eng = Engine(local)
     stream = torch.cuda.Stream(local)
     with torch.cuda.stream(stream):
@@ -336,32 +512,37 @@ def main():
     summary = reduce_summary(summary_stats(torch, ip, og), dist if world > 1 else None)
 
     # ---------------- roofline (fp64 pipe) ----------------
+    # Credit: the units the launch EXECUTED (an instrumented launch of the same
+    # inputs counts them, outside the timed region) x §8d's per-unit costs.
+    counts = eng.count_work(prof, dev)
+    w_exec = executed_work(prof, counts)
     w_og, w_ip = work_model(prof, users)
     peak = eng.fp64_peak()
-    achieved = (w_og + w_ip) / (ms * 1e-3)
-    traffic = None
-    summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(summ):
-        try:
-            traffic = json.load(open(summ)).get("dram_bytes_per_launch_at_1M")
-        except Exception:
-            traffic = None
-    w_pr = pruned_work_model(prof, users) + w_ip
-    achieved_pr = w_pr / (ms * 1e-3)
-    roofline = {"bound": "fp64", "achieved": achieved_pr / 1e12, "peak": peak / 1e12,
-                "unit": "TFLOP/s", "frac": achieved_pr / peak, "traffic": traffic,
-                "work_model": "SURVEY.md §8d per-unit costs (fp64-pipe lane ops, C_ub=19N-13, "
-                              "C_loc=3N+1, C_dp=4) x the units this launch processes: the OG rows "
-                              "truncated to their DP-readable length rlen(i), bounds b <= rlen(i), "
-                              "every chain credited with its full truncated row (DESIGN.md §4)",
-                "ops_per_launch": w_pr,
-                "reference_work": {"ops_per_launch": w_og + w_ip, "achieved": achieved / 1e12,
-                                   "frac": achieved / peak,
-                                   "note": "SURVEY.md §8d W_OG + W_IPSSA: the reference algorithm's "
-                                           "units (every row to M-i users); the launch skips the "
-                                           "rows' unreadable tails exactly, so this rate exceeds "
-                                           "the fp64 peak"},
-                "peak_source": "coinfer_probe_fp64 on this GPU (8 independent DFMA chains/thread, burst)"}
+    props = torch.cuda.get_device_properties(local)
+    sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
+    nominal = props.multi_processor_count * 64 * sm_max * 1e6  # 64 fp64 lanes per SM per clock
+    achieved = w_exec / (ms * 1e-3)
+    live = None if (args.no_ncu or world > 1) else ncu_pass(args)
+    traffic = live.get("dram_bytes") if live else None
+    roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "measured: coinfer_probe_fp64 on this GPU (8 independent DFMA chains "
+                               "per thread, burst) -- MEASURED_PEAKS.json has no fp64 entry",
+                "frac_vs_nominal": achieved / nominal,
+                "nominal_peak": nominal / 1e12,
+                "nominal_source": f"{props.multi_processor_count} SMs x 64 fp64 lanes x {sm_max:.0f} MHz",
+                "work_model": "SURVEY.md §8d per-unit costs (fp64-pipe lane ops: C_ub=19N-13 per "
+                              "(user, chain) evaluation, C_loc=3N+1 per all-local user step, N per "
+                              "chain start, C_dp=4 per DP cell) x the units this launch EXECUTED, "
+                              "counted by the instrumented solve kernel on the same inputs "
+                              "(coinfer_count_work)",
+                "executed_units": counts, "ops_per_launch": w_exec,
+                "ncu_live": live,
+                "reference_work": {"ops_per_launch": w_og + w_ip, "achieved": (w_og + w_ip) / (ms * 1e-3) / 1e12,
+                                   "note": "SURVEY.md §8d W_OG + W_IPSSA: the reference algorithm's own "
+                                           "units (every row to M-i users, every admissible bound); the "
+                                           "launch skips the rows' unreadable tails and dead chains "
+                                           "exactly, so this rate is not a pipe rate"}}
 
     # ---------------- end to end through the C-ABI, host buffers ----------------
     e2e = None
@@ -382,12 +563,23 @@ def main():
         t_e2e = allmax(float(np.mean(times)))
         e2e = {"value": args.n_inst / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
-               "timing": "host wall clock around the synchronous C-ABI call, max over ranks"}
+               "timing": "host wall clock around the synchronous C-ABI call, max over ranks",
+               "outputs": {"ipssa": IP_E2E_FIELDS, "og": OG_E2E_FIELDS},
+               "host_buffers": "inputs page-locked once before the timed region; outputs into "
+                               "reusable page-locked buffers"}
 
     # ---------------- CPU reference baseline (rank 0, N=1) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, _, _ = cpu_reference(prof, users, args.cpu_seconds)
+        cpu["cpu_model"] = cpu_model()
+
+    # ---------------- the other BASELINE configs (driver-clocked) ----------------
+    configs = None
+    if not args.no_configs:
+        del dev, ip, og
+        torch.cuda.empty_cache()
+        configs = other_configs(eng, args, rank, world, allmax, barrier)
 
     if world > 1:
         dist.barrier()
@@ -405,8 +597,8 @@ def main():
                        "parallelism": f"instance shards x{world}",
                        "l2": "inputs 2.8 GB > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk,
-            "summary": summary}))
+            "clocks": clk, "nccl": nccl,
+            "summary": summary, "configs": configs}))
     return 0
 
 

@@ -268,6 +268,15 @@ int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
                         const coinfer_users* users, coinfer_ipssa_out* ipssa,
                         coinfer_og_out* og);
 
+/* Measurement aid (bench.py's roofline): the same fused IP-SSA + OG solve
+   with work counters -- counters[0] OG chain steps ((user, chain)
+   evaluations), [1] IP-SSA chain steps, [2] all-local user steps, [3] b*
+   re-derivation steps, [4] chain starts (start-time recursions), [5] DP
+   cells, [6] instances, [7] reserved.  Decisions are the solver's; M <= 255
+   (the shared-memory path). */
+int coinfer_count_work(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                       coinfer_ipssa_out* ipssa, coinfer_og_out* og, uint64_t* counters);
+
 /* Schedule materialisation on the device (try_fixed_batch:155-185, the
    og stitch :357-386 and normalize).  `solved` holds the decisions of an
    earlier coinfer_ipssa_batch / coinfer_fixed_batch (status, batch_bound,

@@ -135,6 +135,8 @@ PRODUCT_SYMBOLS = {
                                    C.POINTER(OgOut)]),
     "coinfer_sweep_batch": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
                                       C.POINTER(IpssaOut), C.POINTER(OgOut)]),
+    "coinfer_count_work": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),
+                                     C.POINTER(IpssaOut), C.POINTER(OgOut), C.POINTER(C.c_uint64)]),
     "coinfer_ipssa_schedule": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users), _dp,
                                          C.POINTER(IpssaOut), C.POINTER(ScheduleOut)]),
     "coinfer_og_schedule": (C.c_int, [C.c_void_p, C.POINTER(Profile), C.POINTER(Users),

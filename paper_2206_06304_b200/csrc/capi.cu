@@ -40,6 +40,8 @@ struct coinfer_ctx {
   // schedule / baseline / partition calls: staging + scratch (baselines.cu)
   unsigned char* aux = nullptr;
   size_t aux_cap = 0;
+  // coinfer_count_work: device work counters while a counting solve runs
+  unsigned long long* ctr = nullptr;
 };
 
 namespace {
@@ -368,6 +370,7 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
   a.rd = users->rate_down;
   a.pd = users->power_down;
   a.l_ip = deadline;
+  a.ctr = ctx->ctr;
   a.do_ip = ip_in != nullptr;
   a.do_og = og_in != nullptr;
   if (ip_in) a.ip = *ip_in;
@@ -1079,6 +1082,34 @@ int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile, const 
                         coinfer_ipssa_out* ipssa, coinfer_og_out* og) {
   if (!ipssa && !og) return fail(ctx, COINFER_E_ARG, "sweep: no output requested");
   return run(ctx, profile, users, nullptr, nullptr, ipssa, og, Mode::Solve);
+}
+
+int coinfer_count_work(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
+                       coinfer_ipssa_out* ipssa, coinfer_og_out* og, uint64_t* counters) {
+  if (!ctx) return COINFER_E_ARG;
+  if (!counters) return fail(ctx, COINFER_E_ARG, "count_work: null counters");
+  if (!ipssa && !og) return fail(ctx, COINFER_E_ARG, "count_work: no output requested");
+  if (users && users->M > kSmallMaxM)
+    return fail(ctx, COINFER_E_UNSUPPORTED, "count_work: the counting solve covers M <= 255");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  unsigned long long* d = nullptr;
+  e = cudaMalloc(&d, sizeof(unsigned long long) * cfb::CTR_N);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc counters");
+  e = cudaMemsetAsync(d, 0, sizeof(unsigned long long) * cfb::CTR_N, ctx->stream);
+  int rc = e == cudaSuccess ? COINFER_OK : cuda_fail(ctx, e, "memset counters");
+  if (rc == COINFER_OK) {
+    ctx->ctr = d;
+    rc = run(ctx, profile, users, nullptr, nullptr, ipssa, og, Mode::Solve);
+    ctx->ctr = nullptr;
+  }
+  if (rc == COINFER_OK) {
+    e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(counters, d, sizeof(unsigned long long) * cfb::CTR_N, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(ctx, e, "count_work");
+  }
+  cudaFree(d);
+  return rc;
 }
 
 int coinfer_ipssa_schedule(coinfer_ctx* ctx, const coinfer_profile* profile,

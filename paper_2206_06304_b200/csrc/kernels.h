@@ -31,7 +31,12 @@ struct SmallArgs {
   int do_ip, do_og;
   coinfer_ipssa_out ip;
   coinfer_og_out og;
+  // work counters of the counting kernel (solve_count_kernel), else unused:
+  // [0] OG chain steps, [1] IP-SSA chain steps, [2] all-local user steps,
+  // [3] b* re-derivation steps, [4] chain starts, [5] DP cells, [6] instances
+  unsigned long long* ctr;
 };
+enum { CTR_OG = 0, CTR_IP, CTR_LOCAL, CTR_BSTAR, CTR_STARTS, CTR_DP, CTR_INST, CTR_N = 8 };
 
 // One instance's users (global or shared memory), already offset.
 struct InstIn {

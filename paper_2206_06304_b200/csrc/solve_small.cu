@@ -46,7 +46,7 @@ int small_smem_bytes(int M, int N, int W) { return small_smem_bytes_impl(M, N, W
 // or -- for a handful of instances, where SMs would idle -- one CTA of up to
 // 1024 threads per instance, so each instance's chains spread over more
 // lanes (latency).  Same body, same 64-register budget.
-template <int N>
+template <int N, bool COUNT = false>
 __device__ __forceinline__ void solve_batch(const SmallArgs& a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int M = a.M;
@@ -64,7 +64,7 @@ __device__ __forceinline__ void solve_batch(const SmallArgs& a) {
     in.pd = a.pd ? a.pd + base : nullptr;
     in.has_l_ip = a.l_ip != nullptr;
     in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
-    solve_one<N>(a, k, base, M, in, sm, a.L);
+    solve_one<N, false, COUNT>(a, k, base, M, in, sm, a.L);
   }
 }
 
@@ -76,6 +76,12 @@ __global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_small_kernel(SmallA
 template <int N>
 __global__ void __launch_bounds__(1024, 1) solve_wide_kernel(SmallArgs a) {
   solve_batch<N>(a);
+}
+
+// The same solve counting the work units it executes (SmallArgs::ctr).
+template <int N>
+__global__ void __launch_bounds__(256, CFB_SMALL_MINB) solve_count_kernel(SmallArgs a) {
+  solve_batch<N, true>(a);
 }
 
 // fixed_batch_schedule (offline_solvers.hpp:208-214): one CTA per instance.
@@ -174,11 +180,12 @@ int fixed_smem_bytes(int M, int N) { return 8 * M * rec_size(N) + 8 * M + 4 * M 
 // ------------------------------------------------------------ host launch
 template <int N>
 static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, cudaStream_t st) {
+  if (a_in.ctr && threads > 256) threads = 256;  // the counting kernel is built for <= 256
   const int W = threads / 32;
   SmallArgs a = a_in;
   a.L = make_layout(a.M, N, W);
   const int smem = a.L.total;
-  auto kern = threads > 256 ? solve_wide_kernel<N> : solve_small_kernel<N>;
+  auto kern = a.ctr ? solve_count_kernel<N> : threads > 256 ? solve_wide_kernel<N> : solve_small_kernel<N>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

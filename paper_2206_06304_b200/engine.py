@@ -417,6 +417,20 @@ class Engine:
             C.byref(pk.out_ip) if ipssa else None, C.byref(pk.out_og) if og else None))
         return Packed.arrays(pk.out_ip), Packed.arrays(pk.out_og)
 
+    COUNTERS = ["og_chain_steps", "ip_chain_steps", "local_steps", "bstar_steps", "chain_starts",
+                "dp_cells", "instances"]
+
+    def count_work(self, profile, users: Dict):
+        """The fused sweep's executed work units (coinfer_count_work: the
+        instrumented solve kernel, same decisions), as a dict of COUNTERS."""
+        mem = self._mem(users)
+        pk = Packed(profile, users, mem, True, True, f"cuda:{self.device}", ip_fields=["status"],
+                    og_fields=["status"])
+        c = (C.c_uint64 * 8)()
+        self._check(self.lib.coinfer_count_work(self.ctx, C.byref(pk.profile), C.byref(pk.users),
+                                                C.byref(pk.out_ip), C.byref(pk.out_og), c))
+        return dict(zip(self.COUNTERS, [int(x) for x in c]))
+
 
 @dataclass
 class OnlineConfig:

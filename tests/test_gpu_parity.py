@@ -239,3 +239,18 @@ def test_cuda_library_really_loaded(engine):
     assert engine.launches == before + 1
     maps = open("/proc/self/maps").read()
     assert "libcoinfer_b200.so" in maps
+
+
+@pytest.mark.gpu
+def test_count_work_counts_the_same_solve(engine):
+    """coinfer_count_work (bench.py's roofline credit) runs the instrumented
+    solve: deterministic counts, one instance count per instance, chain
+    steps at least the chain starts, and the plain sweep's decisions."""
+    prof = profile_heavy(50)
+    users = sample_batch(300, 50, prof, 0.25, 1.0, seed=77)
+    a = engine.count_work(prof, users)
+    b = engine.count_work(prof, users)
+    assert a == b
+    assert a["instances"] == 300
+    assert a["og_chain_steps"] >= a["chain_starts"] > 0 and a["ip_chain_steps"] > 0
+    assert a["dp_cells"] > 0 and a["bstar_steps"] > 0
