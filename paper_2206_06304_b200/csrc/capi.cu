@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -384,8 +385,17 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
     // warps per CTA to spread each instance's chains wider; a handful (SMs
     // would idle anyway): 16 warps per instance (measured best of 8/16/32 at
     // M = 50..176; COINFER_WIDE overrides, for experiments).
+    // Many instances: large instances (fewer CTAs fit the shared memory)
+    // get more warps per CTA, about 36 / (CTAs per SM), 4..16 -- measured
+    // best at M = 50 (8 CTAs: 4 warps), 75 (5: 7), 100 (3: 12), 150 (1: 16).
     static const int wide = std::getenv("COINFER_WIDE") ? std::atoi(std::getenv("COINFER_WIDE")) : 512;
-    const int threads = Kc >= 1024 ? 128 : Kc >= 148 ? 256 : wide;
+    static const int many = std::getenv("COINFER_THREADS") ? std::atoi(std::getenv("COINFER_THREADS")) : 0;
+    int threads = Kc >= 148 ? 256 : wide;
+    if (Kc >= 1024) {
+      const int smem = cfb::small_smem_bytes((int)M, (int)N, 4);
+      const int ctas = std::max(1, std::min(8, (227 * 1024) / std::max(smem, 1)));
+      threads = many > 0 ? many : 32 * std::max(4, std::min(16, 36 / ctas));
+    }
     return cfb::launch_small(args, threads, grid, st);
   };
   static const bool force_large = std::getenv("COINFER_FORCE_LARGE") != nullptr;  // testing aid

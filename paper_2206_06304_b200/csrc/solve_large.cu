@@ -353,202 +353,333 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   // stage i usually finds column i-1 in shared memory: in the ring, or --
   // when it has a single change point -- in runPM/runRow.  Only a column
   // that overflowed or missed the ring is staged from global memory.
-  double* chgV = a.St;
-  uint16_t* chgR = a.argpm;
-  auto coff = [](int c) { return (long long)c * (c + 1) / 2; };
-  for (int r = tid; r < RING; r += NT) ringOwn[r] = -1;
-  for (int j = tid; j < M; j += NT) rlenS[j] = (uint16_t)a.rlen[j];
-  for (int j = tid; j < M; j += NT) {  // row 0: S[0][j] = G[0][j]
-    const double g = a.G[tri_u(0, j, M)];
-    runPM[j] = g;
-    runRow[j] = 0;
-    ccount[j] = g < INF ? 1 : 0;
-    if (g < INF) {
-      chgV[coff(j)] = g;
-      chgR[coff(j)] = 0;
-    }
-    a.par[tri_u(0, j, M)] = 0xffff;
-  }
-  if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
+  // Fast DP when every row i >= 1 has <= DW useful cells (C4: ~35, peaks in
+  // the 70s).  Column c's useful rows are row 0 and a suffix [q1(c), c]
+  // (c - q < rlen(q) is monotone in q >= 1), so the column prefix minima
+  // live DENSE over that suffix: S0[c] (row 0) below q1(c), then one entry
+  // per row -- the small path's in-place scheme (solve_core.cuh) with O(1)
+  // lookups instead of change-point searches.  Only columns i-1 .. i+DW are
+  // live at stage i, so they sit in a shared-memory ring of DR columns.
+  // Warp 0 runs the stages, one __syncwarp each, the next row's G / pfit
+  // loads in flight.
+  constexpr int DW = 96, DR = 128;
+  int rlmax = 0;
+  for (int j = 1 + tid; j < M; j += NT) rlmax = max(rlmax, a.rlen[j]);
+  rlmax = __reduce_max_sync(kFull, rlmax);
+  if (lane == 0) ired[warp] = rlmax;
   __syncthreads();
-  // S[i][j] for cell (i, j) given G, pfit and column i-1's change points
-  // (V, Rr, nc); appends (i, S) to column j when it is a new strict minimum
-  // (`claim`: short-row stages, whose <= 96 columns are distinct mod RING)
-  auto cell = [&](int i, int j, long long x, double g, int p, const double* V, const uint16_t* Rr, int nc,
-                  bool claim) {
-    double best = INF;
-    int bp = 0xffff;
-    if (g != INF && p > 0) {
-      int lo = 0, hi = nc;  // change points at rows <= p-1
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (Rr[mid] <= p - 1) lo = mid + 1; else hi = mid;
-      }
-      if (lo > 0) {
-        int k = lo - 1;
-        const double cand = __dadd_rn(V[k], g);
-        if (cand != INF) {
-          best = cand;
-          if (k > 0 && __dadd_rn(V[k - 1], g) == best) {  // rounding merged earlier minima
-            int ka = 0;
-            --k;
-            while (ka < k) {
-              const int mid = (ka + k) >> 1;
-              if (__dadd_rn(V[mid], g) == best) k = mid; else ka = mid + 1;
+  rlmax = 0;
+  for (int w = 0; w < NW; ++w) rlmax = max(rlmax, ired[w]);
+  __syncthreads();
+  const bool fastdp = rlmax <= DW;
+  if (fastdp) {
+    double* S0 = reinterpret_cast<double*>(smb);        // [M] row 0: S = G = PM
+    double* ringV = S0 + M;                             // [DR*DW] PM_c over rows q1(c)..
+    double* runV = ringV + DR * DW;                     // [DR] running PM of live columns
+    uint16_t* ringA = reinterpret_cast<uint16_t*>(runV + DR);  // [DR*DW] first position of PM
+    uint16_t* runA = ringA + DR * DW;                   // [DR]
+    uint16_t* q1 = runA + DR;                           // [M] first useful row >= 1 per column (M: none)
+    uint16_t* rlS = q1 + M;                             // [M] useful row lengths
+    for (int j = tid; j < M; j += NT) {
+      const double g = a.G[tri_u(0, j, M)];
+      S0[j] = g;
+      a.par[tri_u(0, j, M)] = 0xffff;
+      q1[j] = (uint16_t)M;
+      rlS[j] = (uint16_t)a.rlen[j];
+    }
+    if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
+    __syncthreads();
+    for (int q = 1 + tid; q < M; q += NT) {  // columns whose first useful row >= 1 is q
+      const int e0 = q == 1 ? 1 : (q - 1) + a.rlen[q - 1], e1 = q + a.rlen[q];
+      for (int c = max(e0, 1); c < e1 && c < M; ++c) q1[c] = (uint16_t)q;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j,
+      // xr(i) = i*M - i(i-1)/2 - i, advanced by M - 1 - i per row
+      const double* __restrict__ G = a.G;
+      const uint16_t* __restrict__ PF = a.pfit;
+      uint16_t* __restrict__ PAR = a.par;
+      double gq[3], gc[3];
+      int pq[3], pc[3];
+      uint32_t xr = (uint32_t)M - 1u;  // row 1
+      auto prefetch = [&](int r, uint32_t xrr) {
+        const int je = r + rlS[r];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int j = r + 32 * c + lane;
+          gq[c] = j < je ? G[xrr + (uint32_t)j] : INF;
+          pq[c] = j < je ? PF[xrr + (uint32_t)j] : 0;
+        }
+      };
+      prefetch(1, xr);
+      for (int i = 1; i < M; ++i, xr += (uint32_t)(M - i)) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          gc[c] = gq[c];
+          pc[c] = pq[c];
+        }
+        if (i + 1 < M) prefetch(i + 1, xr + (uint32_t)(M - 1 - i));  // in flight during this stage
+        const int rl = rlS[i], jend = i + rl;
+        if (lane == 0 && jend < M) a.slast[i] = INF;
+        const int cr = i - 1, q1c = q1[cr];
+        const double s0c = S0[cr];
+        const double* colV = ringV + (cr & (DR - 1)) * DW - q1c;  // colV[r], r >= q1c
+        const uint16_t* colA = ringA + (cr & (DR - 1)) * DW - q1c;
+        // all loads of the stage first (independent), then the decisions, then the stores
+        double rv[3], pmj[3];
+        int pma[3], qjv[3], paj[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int j = min(i + 32 * c + lane, M - 1);
+          const int r = max(pc[c] - 1, 0);
+          rv[c] = r < q1c ? s0c : colV[r];
+          pma[c] = r < q1c ? 0 : colA[r];
+          const int slot = j & (DR - 1), qj = q1[j];
+          qjv[c] = qj;
+          pmj[c] = i == qj ? S0[j] : runV[slot];
+          paj[c] = i == qj ? 0 : runA[slot];
+        }
+        double best[3];
+        int bp[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double g = gc[c];
+          best[c] = INF;
+          bp[c] = 0xffff;
+          if (g != INF && pc[c] > 0) {
+            const double cand = __dadd_rn(rv[c], g);
+            if (cand != INF) {
+              best[c] = cand;
+              int qb = pma[c];
+              if (qb > 0 && __dadd_rn(qb - 1 < q1c ? s0c : colV[qb - 1], g) == cand) {
+                int qa = 0;  // rounding merged an earlier, larger S: first such row
+                --qb;
+                while (qa < qb) {
+                  const int mid = (qa + qb) >> 1;
+                  if (__dadd_rn(mid < q1c ? s0c : colV[mid], g) == cand) qb = mid; else qa = mid + 1;
+                }
+              }
+              bp[c] = qb;
             }
           }
-          bp = Rr[k];
         }
-      }
-    }
-    if (j == M - 1) a.slast[i] = best;
-    a.par[x] = (uint16_t)bp;
-    if (best < runPM[j]) {  // strict: the first position is kept
-      const int n = ccount[j];
-      chgV[coff(j) + n] = best;
-      chgR[coff(j) + n] = (uint16_t)i;
-      const int slot = j & (RING - 1), own = ringOwn[slot];
-      double* rv = ringV + slot * CAP;
-      uint16_t* rr = ringR + slot * CAP;
-      if (own == j) {
-        if (n < CAP) {
-          rv[n] = best;
-          rr[n] = (uint16_t)i;
-        } else {
-          ringOwn[slot] = -1;  // overflow: the column is read from global memory
-        }
-      } else if (claim && n <= 1 && own < i - 1) {  // free, or its column already read
-        if (n == 1) {
-          rv[0] = runPM[j];
-          rr[0] = runRow[j];
-        }
-        rv[n] = best;
-        rr[n] = (uint16_t)i;
-        ringOwn[slot] = j;
-      }
-      ccount[j] = (uint16_t)(n + 1);
-      runPM[j] = best;
-      runRow[j] = (uint16_t)i;
-    }
-  };
-  // column c's change points in shared memory, or nullptr (stage them from global)
-  auto column = [&](int c, int nc, const double*& V, const uint16_t*& Rr) {
-    if (nc <= 1) {
-      V = runPM + c;
-      Rr = runRow + c;
-      return true;
-    }
-    if (ringOwn[c & (RING - 1)] == c) {
-      V = ringV + (c & (RING - 1)) * CAP;
-      Rr = ringR + (c & (RING - 1)) * CAP;
-      return true;
-    }
-    V = colV;
-    Rr = colR;
-    return false;
-  };
-  // Only a row's useful cells j < i + rlen[i] are computed: past them no
-  // prev fits, S = +inf changes no running minimum and no parent is ever
-  // followed.  Rows of <= 96 useful cells (all of them on C4, where rlen
-  // averages ~35 and peaks in the 70s) run on warp 0 alone, synchronised by __syncwarp, with
-  // the next row's G and pfit loads in flight; the other warps skip ahead to
-  // the next long row, which runs on the whole CTA between barriers (<= 8
-  // cells per thread since M <= 8*NT).
-  constexpr int SHORT = CFB_LARGE_SHORT;  // short rows: <= 32*SHORT useful cells
-  int pref = -1;  // warp 0: the row whose first 32*SHORT cells gq/pq hold
-  double gq[SHORT];
-  int pq[SHORT];
-  auto prefetch = [&](int r) {
-    const int je = r + rlenS[r];
-    const long long xr = tri_u(r, r, M) - r;
 #pragma unroll
-    for (int c = 0; c < SHORT; ++c) {
-      const int j = r + 32 * c + lane;
-      gq[c] = j < je ? a.G[xr + j] : INF;
-      pq[c] = j < je ? a.pfit[xr + j] : 0;
-    }
-    pref = r;
-  };
-  for (int i = 1; i < M; ++i) {
-    const int rl = rlenS[i];
-    if (rl <= 32 * SHORT && warp != 0) continue;  // short row: warp 0's
-    const int jend = i + rl;
-    const long long xr = tri_u(i, i, M) - i;  // x(i, j) = xr + j
-    const long long c0 = coff(i - 1);
-    if (rl <= 32 * SHORT) {
-#ifdef CFB_LARGE_TIMING
-      long long t0 = clock64();
-#endif
-      if (pref != i) prefetch(i);
-      double gc[SHORT];
-      int pc[SHORT];
-#pragma unroll
-      for (int c = 0; c < SHORT; ++c) {
-        gc[c] = gq[c];
-        pc[c] = pq[c];
-      }
-      if (i + 1 < M) prefetch(i + 1);  // in flight during this stage
-      if (lane == 0 && jend < M) a.slast[i] = INF;
-      const int nc = ccount[i - 1];
-      const double* V;
-      const uint16_t* Rr;
-      const bool insm = column(i - 1, nc, V, Rr);
-      if (!insm) {
-        for (int q = lane; q < nc; q += 32) {
-          colV[q] = chgV[c0 + q];
-          colR[q] = chgR[c0 + q];
+        for (int c = 0; c < 3; ++c) {
+          const int j = i + 32 * c + lane;
+          if (j >= jend) continue;
+          if (j == M - 1) a.slast[i] = best[c];
+          PAR[xr + (uint32_t)j] = (uint16_t)bp[c];
+          const int slot = j & (DR - 1), qj = qjv[c];
+          const bool lower = best[c] < pmj[c];  // strict: the first position is kept
+          const double npm = lower ? best[c] : pmj[c];
+          const int na = lower ? i : paj[c];
+          runV[slot] = npm;
+          runA[slot] = (uint16_t)na;
+          ringV[slot * DW + (i - qj)] = npm;
+          ringA[slot * DW + (i - qj)] = (uint16_t)na;
         }
         __syncwarp();
       }
-#ifdef CFB_LARGE_TIMING
-      long long t1 = clock64();
-      const double gsink = gc[0] + (double)pc[0];
-      long long t2 = clock64();
-#endif
-#pragma unroll
+    }
+  } else {
+    double* chgV = a.St;
+    uint16_t* chgR = a.argpm;
+    auto coff = [](int c) { return (long long)c * (c + 1) / 2; };
+    for (int r = tid; r < RING; r += NT) ringOwn[r] = -1;
+    for (int j = tid; j < M; j += NT) rlenS[j] = (uint16_t)a.rlen[j];
+    for (int j = tid; j < M; j += NT) {  // row 0: S[0][j] = G[0][j]
+      const double g = a.G[tri_u(0, j, M)];
+      runPM[j] = g;
+      runRow[j] = 0;
+      ccount[j] = g < INF ? 1 : 0;
+      if (g < INF) {
+        chgV[coff(j)] = g;
+        chgR[coff(j)] = 0;
+      }
+      a.par[tri_u(0, j, M)] = 0xffff;
+    }
+    if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
+    __syncthreads();
+    // S[i][j] for cell (i, j) given G, pfit and column i-1's change points
+    // (V, Rr, nc); appends (i, S) to column j when it is a new strict minimum
+    // (`claim`: short-row stages, whose <= 96 columns are distinct mod RING)
+    auto cell = [&](int i, int j, long long x, double g, int p, const double* V, const uint16_t* Rr, int nc,
+                    bool claim) {
+      double best = INF;
+      int bp = 0xffff;
+      if (g != INF && p > 0) {
+        int lo = 0, hi = nc;  // change points at rows <= p-1
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (Rr[mid] <= p - 1) lo = mid + 1; else hi = mid;
+        }
+        if (lo > 0) {
+          int k = lo - 1;
+          const double cand = __dadd_rn(V[k], g);
+          if (cand != INF) {
+            best = cand;
+            if (k > 0 && __dadd_rn(V[k - 1], g) == best) {  // rounding merged earlier minima
+              int ka = 0;
+              --k;
+              while (ka < k) {
+                const int mid = (ka + k) >> 1;
+                if (__dadd_rn(V[mid], g) == best) k = mid; else ka = mid + 1;
+              }
+            }
+            bp = Rr[k];
+          }
+        }
+      }
+      if (j == M - 1) a.slast[i] = best;
+      a.par[x] = (uint16_t)bp;
+      if (best < runPM[j]) {  // strict: the first position is kept
+        const int n = ccount[j];
+        chgV[coff(j) + n] = best;
+        chgR[coff(j) + n] = (uint16_t)i;
+        const int slot = j & (RING - 1), own = ringOwn[slot];
+        double* rv = ringV + slot * CAP;
+        uint16_t* rr = ringR + slot * CAP;
+        if (own == j) {
+          if (n < CAP) {
+            rv[n] = best;
+            rr[n] = (uint16_t)i;
+          } else {
+            ringOwn[slot] = -1;  // overflow: the column is read from global memory
+          }
+        } else if (claim && n <= 1 && own < i - 1) {  // free, or its column already read
+          if (n == 1) {
+            rv[0] = runPM[j];
+            rr[0] = runRow[j];
+          }
+          rv[n] = best;
+          rr[n] = (uint16_t)i;
+          ringOwn[slot] = j;
+        }
+        ccount[j] = (uint16_t)(n + 1);
+        runPM[j] = best;
+        runRow[j] = (uint16_t)i;
+      }
+    };
+    // column c's change points in shared memory, or nullptr (stage them from global)
+    auto column = [&](int c, int nc, const double*& V, const uint16_t*& Rr) {
+      if (nc <= 1) {
+        V = runPM + c;
+        Rr = runRow + c;
+        return true;
+      }
+      if (ringOwn[c & (RING - 1)] == c) {
+        V = ringV + (c & (RING - 1)) * CAP;
+        Rr = ringR + (c & (RING - 1)) * CAP;
+        return true;
+      }
+      V = colV;
+      Rr = colR;
+      return false;
+    };
+    // Only a row's useful cells j < i + rlen[i] are computed: past them no
+    // prev fits, S = +inf changes no running minimum and no parent is ever
+    // followed.  Rows of <= 96 useful cells (all of them on C4, where rlen
+    // averages ~35 and peaks in the 70s) run on warp 0 alone, synchronised by __syncwarp, with
+    // the next row's G and pfit loads in flight; the other warps skip ahead to
+    // the next long row, which runs on the whole CTA between barriers (<= 8
+    // cells per thread since M <= 8*NT).
+    constexpr int SHORT = CFB_LARGE_SHORT;  // short rows: <= 32*SHORT useful cells
+    int pref = -1;  // warp 0: the row whose first 32*SHORT cells gq/pq hold
+    double gq[SHORT];
+    int pq[SHORT];
+    auto prefetch = [&](int r) {
+      const int je = r + rlenS[r];
+      const long long xr = tri_u(r, r, M) - r;
+  #pragma unroll
       for (int c = 0; c < SHORT; ++c) {
-        const int j = i + 32 * c + lane;
-        if (j < jend) cell(i, j, xr + j, gc[c], pc[c], V, Rr, nc, true);
+        const int j = r + 32 * c + lane;
+        gq[c] = j < je ? a.G[xr + j] : INF;
+        pq[c] = j < je ? a.pfit[xr + j] : 0;
       }
-      __syncwarp();
-#ifdef CFB_LARGE_TIMING
-      long long t3 = clock64();
-      if (lane == 0) {
-        g_large_t[0] += t1 - t0;
-        g_large_t[1] += t2 - t1 + (gsink == 12345.0);
-        g_large_t[2] += t3 - t2;
-        g_large_t[3] += 1;
-        g_large_t[4] += insm ? 0 : 1;
+      pref = r;
+    };
+    for (int i = 1; i < M; ++i) {
+      const int rl = rlenS[i];
+      if (rl <= 32 * SHORT && warp != 0) continue;  // short row: warp 0's
+      const int jend = i + rl;
+      const long long xr = tri_u(i, i, M) - i;  // x(i, j) = xr + j
+      const long long c0 = coff(i - 1);
+      if (rl <= 32 * SHORT) {
+  #ifdef CFB_LARGE_TIMING
+        long long t0 = clock64();
+  #endif
+        if (pref != i) prefetch(i);
+        double gc[SHORT];
+        int pc[SHORT];
+  #pragma unroll
+        for (int c = 0; c < SHORT; ++c) {
+          gc[c] = gq[c];
+          pc[c] = pq[c];
+        }
+        if (i + 1 < M) prefetch(i + 1);  // in flight during this stage
+        if (lane == 0 && jend < M) a.slast[i] = INF;
+        const int nc = ccount[i - 1];
+        const double* V;
+        const uint16_t* Rr;
+        const bool insm = column(i - 1, nc, V, Rr);
+        if (!insm) {
+          for (int q = lane; q < nc; q += 32) {
+            colV[q] = chgV[c0 + q];
+            colR[q] = chgR[c0 + q];
+          }
+          __syncwarp();
+        }
+  #ifdef CFB_LARGE_TIMING
+        long long t1 = clock64();
+        const double gsink = gc[0] + (double)pc[0];
+        long long t2 = clock64();
+  #endif
+  #pragma unroll
+        for (int c = 0; c < SHORT; ++c) {
+          const int j = i + 32 * c + lane;
+          if (j < jend) cell(i, j, xr + j, gc[c], pc[c], V, Rr, nc, true);
+        }
+        __syncwarp();
+  #ifdef CFB_LARGE_TIMING
+        long long t3 = clock64();
+        if (lane == 0) {
+          g_large_t[0] += t1 - t0;
+          g_large_t[1] += t2 - t1 + (gsink == 12345.0);
+          g_large_t[2] += t3 - t2;
+          g_large_t[3] += 1;
+          g_large_t[4] += insm ? 0 : 1;
+        }
+  #endif
+        continue;
       }
-#endif
-      continue;
-    }
-    __syncthreads();  // warp 0's short rows are done
-    const int nc = ccount[i - 1];
-    if (tid == 0 && jend < M) a.slast[i] = INF;
-    double gv[8];
-    int pv[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int j = i + tid + c * NT;
-      gv[c] = j < jend ? a.G[xr + j] : INF;
-      pv[c] = j < jend ? a.pfit[xr + j] : 0;
-    }
-    const double* V;
-    const uint16_t* Rr;
-    if (!column(i - 1, nc, V, Rr))
-      for (int q = tid; q < nc; q += NT) {
-        colV[q] = chgV[c0 + q];
-        colR[q] = chgR[c0 + q];
+      __syncthreads();  // warp 0's short rows are done
+      const int nc = ccount[i - 1];
+      if (tid == 0 && jend < M) a.slast[i] = INF;
+      double gv[8];
+      int pv[8];
+  #pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int j = i + tid + c * NT;
+        gv[c] = j < jend ? a.G[xr + j] : INF;
+        pv[c] = j < jend ? a.pfit[xr + j] : 0;
       }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int j = i + tid + c * NT;
-      if (j >= jend) break;
-      cell(i, j, xr + j, gv[c], pv[c], V, Rr, nc, false);
+      const double* V;
+      const uint16_t* Rr;
+      if (!column(i - 1, nc, V, Rr))
+        for (int q = tid; q < nc; q += NT) {
+          colV[q] = chgV[c0 + q];
+          colR[q] = chgR[c0 + q];
+        }
+      __syncthreads();
+  #pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int j = i + tid + c * NT;
+        if (j >= jend) break;
+        cell(i, j, xr + j, gv[c], pv[c], V, Rr, nc, false);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   __syncthreads();
 
@@ -761,7 +892,10 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
   if (a.do_og) large_pfit<<<148 * 8, 256, 0, st>>>(a);
   // running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
-  const int smem = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
+  // fast DP ring: S0 | ring values | running values | ring positions | running positions | q1 | rlen
+  const int smem_fast = 8 * M + 128 * 96 * 8 + 128 * 8 + 128 * 96 * 2 + 128 * 2 + 2 * 2 * M;
+  const int smem_old = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
+  const int smem = smem_fast > smem_old ? smem_fast : smem_old;
   if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
   cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -19,8 +19,8 @@ if [ -n "$C4" ]; then
   ncu -i $R/c4.ncu-rep --page raw --csv > $R/c4_raw.csv 2>/dev/null
   python scripts/ncu_kernels.py $R/c4_raw.csv > gpurun_out/${TAG}_c4.txt 2>&1
   python scripts/ncu_linedump.py $R/c4.ncu-rep > gpurun_out/${TAG}_c4_lines.csv 2>&1
-  ncu --set full --import-source on --clock-control none -k regex:online -c 1 -o $R/c5 \
-      python scripts/bench_online.py 256 20000 light > gpurun_out/${TAG}_c5.log 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:online --launch-skip 1 -c 1 -o $R/c5 \
+      python scripts/bench_online.py 4096 3000 light > gpurun_out/${TAG}_c5.log 2>&1
   bash scripts/ncu_summary.sh $R/c5.ncu-rep > gpurun_out/${TAG}_c5.txt 2>&1
   python scripts/ncu_linedump.py $R/c5.ncu-rep > gpurun_out/${TAG}_c5_lines.csv 2>&1
 fi

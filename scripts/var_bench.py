@@ -19,8 +19,10 @@ for M, K, light in [(50, 1024, False), (20, 512, False), (14, 256, True), (100, 
     prof = profile_light(M) if light else profile_heavy(M)
     u = sample_batch(K, M, prof, 0.05 if light else 0.25, 0.2 if light else 1.0, seed=M + 1000)
     ip, og = eng.sweep(prof, u)
-    ck.assert_same_ip(ip, ck.oracle_ipssa(prof, u), where=f"M={M}")
+    ipx = ck.oracle_ipssa(prof, u)
+    ck.assert_same_ip(ip, ipx, where=f"M={M}")
     ck.assert_same_og(og, ck.oracle_og(prof, u), where=f"M={M}")
+    ck.assert_same_ip(eng.ipssa(prof, u), ipx, where=f"M={M} ipssa only")
 prof = profile_heavy(50)
 K = int(os.environ.get("VB_K", "1000000"))
 seeds = sub_seed(1, 1, np.arange(K, dtype=np.uint64))
