@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -35,15 +37,41 @@ struct coinfer_ctx {
   cudaStream_t pipe[2] = {nullptr, nullptr};
   unsigned char* ws2[2] = {nullptr, nullptr};
   size_t ws2_cap[2] = {0, 0};
-  // large-instance path workspace (G/S triangles etc.)
-  unsigned char* big = nullptr;
-  size_t big_cap = 0;
+  // large-instance path: instances of a batch run round-robin on up to
+  // kLargeStreams streams, each with its own workspace (G/S triangles etc.)
+  static constexpr int kLargeStreams = 16;
+  cudaStream_t lst[kLargeStreams] = {};
+  cudaEvent_t lev[kLargeStreams] = {};
+  unsigned char* big[kLargeStreams] = {};
+  size_t big_cap[kLargeStreams] = {};
+  cudaEvent_t lstart = nullptr;
   // schedule / baseline / partition calls: staging + scratch (baselines.cu)
   unsigned char* aux = nullptr;
   size_t aux_cap = 0;
   // coinfer_count_work: device work counters while a counting solve runs
   unsigned long long* ctr = nullptr;
 };
+
+namespace cfb {
+cudaError_t ensure_smem(const void* f, int smem, bool carveout) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> smem set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({f, dev});
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (carveout) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  done[{f, dev}] = smem;
+  return cudaSuccess;
+}
+}  // namespace cfb
 
 namespace {
 
@@ -251,56 +279,83 @@ constexpr int kSmallMaxM = 255;  // u8 group/bound indices in shared memory
 // Instances too large for one CTA's shared memory: the multi-kernel path of
 // solve_large.cu, one instance at a time.  `a` carries device pointers.
 int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st) {
+  // One instance = 6 dependent launches (solve_large.cu).  A batch runs its
+  // instances round-robin on up to kLargeStreams streams, each with its own
+  // workspace (bounded to ~4 GB in total), ordered after everything already
+  // queued on `st`; `st` then waits for all of them.
   const int M = a.M, N = a.P.N;
   const size_t need = cfb::large_ws_bytes(M, N);
-  if (need > ctx->big_cap) {
-    cudaStreamSynchronize(st);
-    if (ctx->big) cudaFree(ctx->big);
-    ctx->big = nullptr;
-    ctx->big_cap = 0;
-    cudaError_t e = cudaMalloc(&ctx->big, need);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(large workspace)");
-    ctx->big_cap = need;
+  int S = (int)std::min<int64_t>(coinfer_ctx::kLargeStreams, std::max<int64_t>(1, a.n_inst));
+  S = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, ((size_t)4 << 30) / std::max<size_t>(need, 1)));
+  cudaError_t e;
+  if (!ctx->lstart) {
+    e = cudaEventCreateWithFlags(&ctx->lstart, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventCreate");
+  }
+  e = cudaEventRecord(ctx->lstart, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaEventRecord");
+  for (int w = 0; w < S; ++w) {
+    if (!ctx->lst[w]) {
+      e = cudaStreamCreateWithFlags(&ctx->lst[w], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->lev[w], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "large-path stream");
+    }
+    if (need > ctx->big_cap[w]) {
+      cudaStreamSynchronize(ctx->lst[w]);
+      if (ctx->big[w]) cudaFree(ctx->big[w]);
+      ctx->big[w] = nullptr;
+      ctx->big_cap[w] = 0;
+      e = cudaMalloc(&ctx->big[w], need);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(large workspace)");
+      ctx->big_cap[w] = need;
+    }
+    e = cudaStreamWaitEvent(ctx->lst[w], ctx->lstart, 0);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamWaitEvent");
   }
   const size_t T = (size_t)M * (M + 1) / 2;
-  unsigned char* w = ctx->big;
-  auto take = [&](size_t bytes) {
-    unsigned char* p = w;
-    w += (bytes + 255) & ~size_t(255);
-    return p;
+  auto workspace = [&](int w) {
+    unsigned char* p = ctx->big[w];
+    auto take = [&](size_t bytes) {
+      unsigned char* q = p;
+      p += (bytes + 255) & ~size_t(255);
+      return q;
+    };
+    cfb::LargeArgs L;
+    std::memset(&L, 0, sizeof L);
+    L.P = a.P;
+    L.lat = a.lat;
+    L.M = M;
+    L.do_ip = a.do_ip;
+    L.do_og = a.do_og;
+    L.G = reinterpret_cast<double*>(take(8 * T));
+    L.St = reinterpret_cast<double*>(take(8 * T));
+    L.bstar = reinterpret_cast<uint16_t*>(take(2 * T));
+    L.par = reinterpret_cast<uint16_t*>(take(2 * T));
+    L.pfit = reinterpret_cast<uint16_t*>(take(2 * T));
+    L.argpm = reinterpret_cast<uint16_t*>(take(2 * T));
+    L.slast = reinterpret_cast<double*>(take(8 * (size_t)M));
+    L.rec = reinterpret_cast<double*>(take((size_t)M * cfb::rec_size(N) * 8));
+    L.dls = reinterpret_cast<double*>(take(8 * (size_t)M));
+    L.sumlat = reinterpret_cast<double*>(take(8 * ((size_t)M + 2)));
+    L.fpos = reinterpret_cast<double*>(take(8 * (size_t)M));
+    L.genergy = reinterpret_cast<double*>(take(8 * (size_t)M));
+    L.ipres = reinterpret_cast<double*>(take(8));
+    L.order = reinterpret_cast<int*>(take(4 * (size_t)M));
+    L.rank = reinterpret_cast<int*>(take(4 * (size_t)M));
+    L.b0 = reinterpret_cast<int*>(take(4 * ((size_t)M + 2)));
+    L.spos = reinterpret_cast<int*>(take(4 * (size_t)M));
+    L.gid = reinterpret_cast<int*>(take(4 * (size_t)M));
+    L.rlen = reinterpret_cast<int*>(take(4 * (size_t)M));
+    L.status = reinterpret_cast<int*>(take(4));
+    L.simple = reinterpret_cast<int*>(take(4));
+    L.ipb = reinterpret_cast<uint16_t*>(take(4));
+    L.ip = a.ip;
+    L.og = a.og;
+    return L;
   };
-  cfb::LargeArgs L;
-  std::memset(&L, 0, sizeof L);
-  L.P = a.P;
-  L.lat = a.lat;
-  L.M = M;
-  L.do_ip = a.do_ip;
-  L.do_og = a.do_og;
-  L.G = reinterpret_cast<double*>(take(8 * T));
-  L.St = reinterpret_cast<double*>(take(8 * T));
-  L.bstar = reinterpret_cast<uint16_t*>(take(2 * T));
-  L.par = reinterpret_cast<uint16_t*>(take(2 * T));
-  L.pfit = reinterpret_cast<uint16_t*>(take(2 * T));
-  L.argpm = reinterpret_cast<uint16_t*>(take(2 * T));
-  L.slast = reinterpret_cast<double*>(take(8 * (size_t)M));
-  L.rec = reinterpret_cast<double*>(take((size_t)M * cfb::rec_size(N) * 8));
-  L.dls = reinterpret_cast<double*>(take(8 * (size_t)M));
-  L.sumlat = reinterpret_cast<double*>(take(8 * ((size_t)M + 2)));
-  L.fpos = reinterpret_cast<double*>(take(8 * (size_t)M));
-  L.genergy = reinterpret_cast<double*>(take(8 * (size_t)M));
-  L.ipres = reinterpret_cast<double*>(take(8));
-  L.order = reinterpret_cast<int*>(take(4 * (size_t)M));
-  L.rank = reinterpret_cast<int*>(take(4 * (size_t)M));
-  L.b0 = reinterpret_cast<int*>(take(4 * ((size_t)M + 2)));
-  L.spos = reinterpret_cast<int*>(take(4 * (size_t)M));
-  L.gid = reinterpret_cast<int*>(take(4 * (size_t)M));
-  L.rlen = reinterpret_cast<int*>(take(4 * (size_t)M));
-  L.status = reinterpret_cast<int*>(take(4));
-  L.simple = reinterpret_cast<int*>(take(4));
-  L.ipb = reinterpret_cast<uint16_t*>(take(4));
-  L.ip = a.ip;
-  L.og = a.og;
   for (int64_t k = 0; k < a.n_inst; ++k) {
+    const int w = (int)(k % S);
+    cfb::LargeArgs L = workspace(w);
     const size_t base = (size_t)k * M;
     L.k = k;
     L.base = base;
@@ -313,17 +368,15 @@ int run_large_device(coinfer_ctx* ctx, const cfb::SmallArgs& a, cudaStream_t st)
     L.dl = a.dl + base;
     L.rd = a.rd ? a.rd + base : nullptr;
     L.pd = a.pd ? a.pd + base : nullptr;
-    if (a.l_ip) {  // a device pointer: read it inside the kernels would need a copy
-      double v;
-      cudaError_t e = cudaMemcpyAsync(&v, a.l_ip + k, 8, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "read IP-SSA deadline");
-      L.l_ip = v;
-      L.has_l_ip = 1;
-    }
-    cudaError_t e = cfb::launch_large(L, st);
+    L.l_ip_dev = a.l_ip ? a.l_ip + k : nullptr;  // read on the device
+    e = cfb::launch_large(L, ctx->lst[w]);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "large-instance launch");
     ctx->launches += 6;
+  }
+  for (int w = 0; w < S; ++w) {
+    e = cudaEventRecord(ctx->lev[w], ctx->lst[w]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->lev[w], 0);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "large-path join");
   }
   return COINFER_OK;
 }
@@ -405,12 +458,10 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
       (size_t)cfb::fixed_smem_bytes((int)M, (int)N) > 227 * 1024)
     return fail(ctx, COINFER_E_UNSUPPORTED, "fixed_batch: instance does not fit in shared memory");
   if (large && mode != Mode::Fixed) {
-    // one instance at a time through solve_large.cu; host batches are staged whole
+    // solve_large.cu, instances spread over the large-path streams; host
+    // batches are staged whole (the workspaces are per worker stream, so
+    // successive calls order themselves on those streams)
     if (users->mem == COINFER_MEM_DEVICE) return run_large_device(ctx, a, ctx->stream);
-    // the large workspace (ctx->big) is shared with device-memory calls on
-    // ctx->stream, which may still be running: order this call after them
-    e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "synchronize before large host call");
     Stager st{ctx};
     plan_in(st, a.fmin, K * M);
     plan_in(st, a.fmax, K * M);
@@ -829,7 +880,13 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_lat) cudaFree(ctx->d_lat);
-  if (ctx->big) cudaFree(ctx->big);
+  for (int w = 0; w < coinfer_ctx::kLargeStreams; ++w) {
+    if (ctx->lst[w]) cudaStreamSynchronize(ctx->lst[w]);
+    if (ctx->big[w]) cudaFree(ctx->big[w]);
+    if (ctx->lev[w]) cudaEventDestroy(ctx->lev[w]);
+    if (ctx->lst[w]) cudaStreamDestroy(ctx->lst[w]);
+  }
+  if (ctx->lstart) cudaEventDestroy(ctx->lstart);
   if (ctx->aux) cudaFree(ctx->aux);
   for (int i = 0; i < 2; ++i) {
     if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);

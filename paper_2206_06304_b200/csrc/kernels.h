@@ -77,6 +77,7 @@ struct LargeArgs {
   const double *fmin, *fmax, *kappa, *ru, *pu, *arr, *dl, *rd, *pd;  // this instance
   double l_ip;
   int has_l_ip, do_ip, do_og;
+  const double* l_ip_dev;  // else: this instance's IP-SSA deadline in device memory (read on the device)
   int64_t k;    // output instance index
   size_t base;  // output row (k * M)
   // workspace
@@ -150,6 +151,11 @@ int small_smem_bytes(int M, int N, int W);
 int online_smem_bytes(int M, int N);
 size_t large_ws_bytes(int M, int N);
 cudaError_t launch_large(const LargeArgs& a, cudaStream_t st);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize [, carveout 100%]) for
+// kernel f on the current device, only when the request grows (a cached
+// per-(kernel, device) high-water mark: single-instance calls pay no
+// attribute round trips).
+cudaError_t ensure_smem(const void* f, int smem, bool carveout = false);
 cudaError_t launch_online(const OnlineArgs& a, int grid, cudaStream_t st);
 int fixed_smem_bytes(int M, int N);
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st);

@@ -727,13 +727,13 @@ static cudaError_t launch_online_n(const OnlineArgs& a_in, int grid, cudaStream_
   static const bool serial = std::getenv("COINFER_ONLINE_SERIAL") != nullptr;  // testing aid
   if (a.M <= 32 && !serial) {
     const int smem = online_warp_smem_bytes(a.M, N);
-    cudaError_t e = cudaFuncSetAttribute(online_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = ensure_smem((const void*)online_warp_kernel<N>, smem);
     if (e != cudaSuccess) return e;
     online_warp_kernel<N><<<grid, 32, smem, st>>>(a);
     return cudaGetLastError();
   }
   const int smem = online_smem_bytes(a.M, N);
-  cudaError_t e = cudaFuncSetAttribute(online_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_smem((const void*)online_kernel<N>, smem);
   if (e != cudaSuccess) return e;
   online_kernel<N><<<grid, 32, smem, st>>>(a);
   return cudaGetLastError();

@@ -38,6 +38,11 @@ __device__ __forceinline__ long long tri_u(long long i, long long j, long long M
 
 }  // namespace
 
+// The IP-SSA deadline: the caller's (host value or device pointer), else `dflt`.
+__device__ __forceinline__ double ip_deadline(const LargeArgs& a, double dflt) {
+  return a.l_ip_dev ? *a.l_ip_dev : (a.has_l_ip ? a.l_ip : dflt);
+}
+
 template <int N>
 __global__ void large_prep(LargeArgs a) {
   using R = Rec<N>;
@@ -77,7 +82,7 @@ __global__ void large_rows(LargeArgs a) {
   if (q >= Q) return;
   const bool isip = q < nip;
   const int len = isip ? M : M - (q - nip);
-  const double d = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[q - nip];
+  const double d = isip ? ip_deadline(a, a.dls[0]) : a.dls[q - nip];
   a.b0[q] = first_infeasible<N>(a.lat, a.P.bmax, d, len);
   if (!isip) {
     // useful length (solve_core.cuh, "Useful cells"): cells (row, j) with
@@ -105,7 +110,7 @@ __device__ __forceinline__ void grow_row(const LargeArgs& a, int q, int lane) {
   const int row = q - nip;
   const int len = isip ? M : M - row;
   const int b0q = a.b0[q];
-  const double dlq = isip ? (a.has_l_ip ? a.l_ip : a.dls[0]) : a.dls[row];
+  const double dlq = isip ? ip_deadline(a, a.dls[0]) : a.dls[row];
   const double INF = dinf();
   double* gE = isip ? a.ipres : a.G + tri_u(row, row, M);
   uint16_t* gB = isip ? a.ipb : a.bstar + tri_u(row, row, M);
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
     if (ipE == INF) {
       if (tid == 0 && a.ip.status) a.ip.status[a.k] = COINFER_ST_INFEASIBLE;
     } else {
-      const double l_ip = a.has_l_ip ? a.l_ip : dls[0];
+      const double l_ip = ip_deadline(a, dls[0]);
       const bool pipe = ipbv < a.b0[0];
       double s[N];
       if (pipe) start_times<N>(a.lat, P.bmax, l_ip, ipbv, s);
@@ -880,7 +885,8 @@ __global__ void large_pfit(LargeArgs a) {
 __global__ void large_init(LargeArgs a) {
   // Scenario::check tests the table length before any user (core_model.hpp:86-87)
   *a.status = a.P.bmax < a.M ? COINFER_ST_SHORT_TABLE : INT_MAX;
-  *a.simple = fast_div_profile(a.P) && (!a.do_ip || !a.has_l_ip || fast_div_deadline(a.l_ip)) ? 1 : 0;
+  const bool given = a.has_l_ip || a.l_ip_dev;
+  *a.simple = fast_div_profile(a.P) && (!a.do_ip || !given || fast_div_deadline(ip_deadline(a, 0.0))) ? 1 : 0;
 }
 
 template <int N>
@@ -890,14 +896,18 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   large_prep<N><<<(M + 256) / 256, 256, 0, st>>>(a);
   large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
-  if (a.do_og) large_pfit<<<148 * 8, 256, 0, st>>>(a);
+  if (a.do_og) {
+    const long long T = (long long)M * (M + 1) / 2;
+    const int g = (int)((T + 255) / 256 < 148 * 8 ? (T + 255) / 256 : 148 * 8);
+    large_pfit<<<g, 256, 0, st>>>(a);
+  }
   // running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
   // fast DP ring: S0 | ring values | running values | ring positions | running positions | q1 | rlen
   const int smem_fast = 8 * M + 128 * 96 * 8 + 128 * 8 + 128 * 96 * 2 + 128 * 2 + 2 * 2 * M;
   const int smem_old = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
   const int smem = smem_fast > smem_old ? smem_fast : smem_old;
   if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
-  cudaError_t e = cudaFuncSetAttribute(large_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_smem((const void*)large_finish<N>, smem);
   if (e != cudaSuccess) return e;
   large_finish<N><<<1, 1024, smem, st>>>(a);
   return cudaGetLastError();

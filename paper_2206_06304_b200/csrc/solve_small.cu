@@ -186,9 +186,7 @@ static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, 
   a.L = make_layout(a.M, N, W);
   const int smem = a.L.total;
   auto kern = a.ctr ? solve_count_kernel<N> : threads > 256 ? solve_wide_kernel<N> : solve_small_kernel<N>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t e = ensure_smem((const void*)kern, smem, true);
   if (e != cudaSuccess) return e;
   kern<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
@@ -197,8 +195,7 @@ static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, 
 template <int N>
 static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st) {
   const int smem = fixed_smem_bytes(a.M, N);
-  cudaError_t e = cudaFuncSetAttribute(fixed_batch_kernel<N>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_smem((const void*)fixed_batch_kernel<N>, smem);
   if (e != cudaSuccess) return e;
   fixed_batch_kernel<N><<<grid, 128, smem, st>>>(a, b);
   return cudaGetLastError();

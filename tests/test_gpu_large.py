@@ -43,6 +43,27 @@ def test_large_loose_deadlines(engine):
     ck.assert_same_og(og, ck.oracle_og(prof, users), where="large loose og")
 
 
+def test_large_batch_streams_and_device_deadlines(engine):
+    """A batch of large instances runs round-robin on the large-path streams
+    (one workspace each): every instance equals the oracle, from host and
+    from device memory, with per-instance IP-SSA deadlines read on the device."""
+    import torch
+    M, K = 200, 20
+    prof = profile_heavy(M)
+    users = sample_batch(K, M, prof, 0.25, 1.0, seed=21)
+    dl = users["deadline"].min(axis=1) * np.linspace(1.0, 1.4, K)
+    ipx = ck.oracle_ipssa(prof, users, deadline=dl)
+    ogx = ck.oracle_og(prof, users)
+    ck.assert_same_ip(engine.ipssa(prof, users, deadline=dl), ipx, where="large batch ipssa (host)")
+    ck.assert_same_og(engine.og(prof, users), ogx, where="large batch og (host)")
+    dev = {k: torch.as_tensor(v, device="cuda") for k, v in users.items()}
+    ipd = engine.ipssa(prof, dev, deadline=torch.as_tensor(dl, device="cuda"))
+    ogd = engine.og(prof, dev)
+    engine.synchronize()
+    ck.assert_same_ip({k: v.cpu().numpy() for k, v in ipd.items()}, ipx, where="large batch ipssa (device)")
+    ck.assert_same_og({k: v.cpu().numpy() for k, v in ogd.items()}, ogx, where="large batch og (device)")
+
+
 def test_large_light_profile(engine):
     prof = profile_light(400)
     users = sample_batch(1, 400, prof, 0.05, 0.2, seed=5)
