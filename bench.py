@@ -193,6 +193,7 @@ def cpu_model():
     return None
 
 
+NCU_KERNELS = "regex:solve_(small|pipe)_kernel"  # the dominant kernel: one C3 solve launch
 NCU_METRICS = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
                "smsp__issue_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum",
                "dram__bytes_write.sum", "smsp__inst_executed.sum"]
@@ -208,7 +209,7 @@ def ncu_pass(args):
     if not os.path.exists(ncu):
         return None
     out = f"/tmp/coinfer_ncu_{os.getpid()}.csv"
-    cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "-k", "regex:solve_small",
+    cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "-k", NCU_KERNELS,
            "-c", "1", "--csv", "--log-file", out, sys.executable, os.path.abspath(__file__), "--ncu-child",
            "--n-inst", str(args.n_inst), "--M", str(args.M), "--seed", str(args.seed)]
     try:
@@ -216,19 +217,21 @@ def ncu_pass(args):
         import csv
         lines = [l for l in open(out) if not l.startswith("==")]
         vals = {}
+        kname = None
         for r in csv.DictReader(lines):
+            kname = kname or r.get("Kernel Name")
             scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
                      "ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
                      "msecond": 1.0, "s": 1e3, "second": 1e3}.get(r["Metric Unit"], 1.0)
             vals[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * scale
         os.unlink(out)
-        return {"kernel": "cfb::solve_small_kernel<4> (1 launch, the bench's inputs)",
+        return {"kernel": f"{kname} (1 launch, the bench's inputs)",
                 "fp64_pipe_active_pct": vals.get(NCU_METRICS[1]),
                 "issue_active_pct": vals.get(NCU_METRICS[2]),
                 "dram_bytes": vals.get(NCU_METRICS[3], 0.0) + vals.get(NCU_METRICS[4], 0.0),
                 "warp_instructions": vals.get(NCU_METRICS[5]),
                 "gpu_time_ms_under_ncu": vals.get(NCU_METRICS[0]),
-                "command": "ncu --metrics " + ",".join(NCU_METRICS) + " --clock-control none -k regex:solve_small -c 1"}
+                "command": "ncu --metrics " + ",".join(NCU_METRICS) + f" --clock-control none -k {NCU_KERNELS} -c 1"}
     except Exception as ex:  # noqa: BLE001 -- a measurement aid, never fatal
         return {"error": str(ex)[:200]}
 

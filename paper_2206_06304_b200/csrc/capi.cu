@@ -50,6 +50,11 @@ struct coinfer_ctx {
   size_t aux_cap = 0;
   // coinfer_count_work: device work counters while a counting solve runs
   unsigned long long* ctr = nullptr;
+  // pipelined kernel: instance claim counters, one per launch in rotation
+  // (each launch zeroes its own on its stream first)
+  static constexpr int kClaims = 64;
+  unsigned long long* claim = nullptr;
+  int claim_next = 0;
 };
 
 namespace cfb {
@@ -274,7 +279,10 @@ void patch_og_out(unsigned char* b, coinfer_og_out& o) {
 #ifndef CFB_E2E_MINCHUNK
 #define CFB_E2E_MINCHUNK 32768  // instances per chunk, at least (measured: 8 / 16 / 32 chunks of 1M: 8.17 / 8.40 / 8.53M/s e2e)
 #endif
-constexpr int kSmallMaxM = 255;  // u8 group/bound indices in shared memory
+constexpr int kSmallMaxM = 255;
+#ifndef CFB_PIPE_MAXM
+#define CFB_PIPE_MAXM 64  // largest M run by the pipelined kernel (measured: see DESIGN.md §4)
+#endif  // u8 group/bound indices in shared memory
 
 // Instances too large for one CTA's shared memory: the multi-kernel path of
 // solve_large.cu, one instance at a time.  `a` carries device pointers.
@@ -441,6 +449,21 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
     // Many instances: large instances (fewer CTAs fit the shared memory)
     // get more warps per CTA, about 36 / (CTAs per SM), 4..16 -- measured
     // best at M = 50 (8 CTAs: 4 warps), 75 (5: 7), 100 (3: 12), 150 (1: 16).
+    // Many small instances: the pipelined kernel (two instances per CTA,
+    // G-phase warps apart from front/tail warps) when two buffers fit.
+    static const char* pipe_env = std::getenv("COINFER_PIPE");
+    static const int pipe_maxm = std::getenv("COINFER_PIPE_MAXM") ? std::atoi(std::getenv("COINFER_PIPE_MAXM"))
+                                                                   : CFB_PIPE_MAXM;
+    if (!args.ctr && Kc >= 2048 && (int)M <= pipe_maxm && cfb::pipe_fits((int)M, (int)N) &&
+        !(pipe_env && pipe_env[0] == '0')) {
+      if (!ctx->claim) {
+        cudaError_t e = cudaMalloc(&ctx->claim, sizeof(unsigned long long) * coinfer_ctx::kClaims);
+        if (e != cudaSuccess) return e;
+      }
+      cfb::SmallArgs ap = args;
+      ap.claim = ctx->claim + (ctx->claim_next++ % coinfer_ctx::kClaims);
+      return cfb::launch_pipe(ap, st);
+    }
     static const int wide = std::getenv("COINFER_WIDE") ? std::atoi(std::getenv("COINFER_WIDE")) : 512;
     static const int many = std::getenv("COINFER_THREADS") ? std::atoi(std::getenv("COINFER_THREADS")) : 0;
     int threads = Kc >= 148 ? 256 : wide;
@@ -888,6 +911,7 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   }
   if (ctx->lstart) cudaEventDestroy(ctx->lstart);
   if (ctx->aux) cudaFree(ctx->aux);
+  if (ctx->claim) cudaFree(ctx->claim);
   for (int i = 0; i < 2; ++i) {
     if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);
     if (ctx->ws2[i]) cudaFree(ctx->ws2[i]);

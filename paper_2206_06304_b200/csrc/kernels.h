@@ -35,6 +35,8 @@ struct SmallArgs {
   // [0] OG chain steps, [1] IP-SSA chain steps, [2] all-local user steps,
   // [3] b* re-derivation steps, [4] chain starts, [5] DP cells, [6] instances
   unsigned long long* ctr;
+  // instance claim counter of the pipelined kernel (zeroed before each launch)
+  unsigned long long* claim;
 };
 enum { CTR_OG = 0, CTR_IP, CTR_LOCAL, CTR_BSTAR, CTR_STARTS, CTR_DP, CTR_INST, CTR_N = 8 };
 
@@ -159,6 +161,11 @@ cudaError_t ensure_smem(const void* f, int smem, bool carveout = false);
 cudaError_t launch_online(const OnlineArgs& a, int grid, cudaStream_t st);
 int fixed_smem_bytes(int M, int N);
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st);
+// The pipelined persistent kernel (solve_small.cu: solve_pipe_kernel); a.claim
+// must be set.  Returns cudaErrorInvalidValue when two instance buffers of
+// this size do not fit (the caller then uses launch_small).
+cudaError_t launch_pipe(const SmallArgs& a, cudaStream_t st);
+bool pipe_fits(int M, int N);
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
 
 #ifdef CFB_ONLY_N  // development builds: one sub-task count only (fast compiles)

@@ -175,6 +175,151 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
   }
 }
 
+
+// Pipelined persistent kernel.  Per instance the fused solve is a latency-
+// bound front (check, sort, hoist, row layout, DP feasibility), the
+// issue-bound G table, and a latency-bound tail (IP-SSA output, DP,
+// backtrack, b*, stitch) with a barrier per DP stage; in the one-CTA-per-
+// instance kernel every warp of the CTA sits through the front and tail.
+// Here a CTA holds two instance buffers and splits its warps: CFB_PIPE_GW
+// warps run only G phases, alternating buffers, while CFB_PIPE_LW warps run
+// the tail of one instance and then the front of the next into the same
+// buffer.  Named barriers 1 (G team) and 2 (front/tail team) are the teams'
+// own; the hand-offs are mbarriers: F[b] "front done in buffer b" (every
+// front/tail thread arrives, G warps wait on its phase) and D[b] "G done in
+// buffer b" (every G thread arrives, the front/tail team waits).  G warps
+// are not synchronised with each other: one that runs out of chains starts
+// the next instance as soon as its front is done.  Instances are claimed
+// from a global counter, so CTAs stay busy to the end.
+#ifndef CFB_PIPE_GW
+#define CFB_PIPE_GW 6
+#endif
+#ifndef CFB_PIPE_LW
+#define CFB_PIPE_LW 2
+#endif
+constexpr int kPipeGT = 32 * CFB_PIPE_GW, kPipeLT = 32 * CFB_PIPE_LW, kPipeT = kPipeGT + kPipeLT;
+
+__device__ __forceinline__ void mb_init(uint32_t addr, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" : : "r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint32_t addr) {  // release
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" : : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t addr, unsigned parity) {  // acquire
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}"
+      : : "r"(addr), "r"(parity) : "memory");
+}
+
+__host__ __device__ inline int pipe_buf_bytes(int M, int N) { return (make_layout(M, N, 4).total + 127) & ~127; }
+
+#ifdef CFB_PIPE_PROF  // development: cycles each team spends waiting on the other
+static __device__ unsigned long long g_pipe_cyc[4];  // G wait, G busy, L wait, L busy (per warp-0 lane 0 of each team)
+extern "C" int coinfer_debug_pipe_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_pipe_cyc, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0};
+    cudaMemcpyToSymbol(g_pipe_cyc, z, sizeof z);
+  }
+  return 0;
+}
+#define PIPE_T0 const long long _t0 = clock64();
+#define PIPE_ACC(i) if ((threadIdx.x & 31) == 0 && (threadIdx.x == 0 || threadIdx.x == kPipeGT)) atomicAdd(&g_pipe_cyc[i], (unsigned long long)(clock64() - _t0));
+#else
+#define PIPE_T0
+#define PIPE_ACC(i)
+#endif
+
+template <int N>
+__global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ long long kb[2];  // instance in buffer b, -1: none (stop)
+  __shared__ __align__(8) unsigned long long mbar[4];  // F[0], F[1], D[0], D[1]
+  const int M = a.M;
+  const int bufb = pipe_buf_bytes(M, N);
+  const int w = threadIdx.x >> 5;
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
+  auto F = [&](int b) { return mb0 + 8u * (uint32_t)b; };
+  auto D = [&](int b) { return mb0 + 16u + 8u * (uint32_t)b; };
+  if (threadIdx.x == 0) {
+    mb_init(F(0), kPipeLT);
+    mb_init(F(1), kPipeLT);
+    mb_init(D(0), kPipeGT);
+    mb_init(D(1), kPipeGT);
+  }
+  __syncthreads();
+  auto input = [&](long long k) {
+    const size_t base = (size_t)k * M;
+    InstIn in;
+    in.fmin = a.fmin + base;
+    in.fmax = a.fmax + base;
+    in.kappa = a.kappa + base;
+    in.ru = a.ru + base;
+    in.pu = a.pu + base;
+    in.arr = a.arr + base;
+    in.dl = a.dl + base;
+    in.rd = a.rd ? a.rd + base : nullptr;
+    in.pd = a.pd ? a.pd + base : nullptr;
+    in.has_l_ip = a.l_ip != nullptr;
+    in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
+    return in;
+  };
+  if (w < CFB_PIPE_GW) {  // G team
+    const Team T{(int)threadIdx.x, kPipeGT, w, 1};
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      {
+        PIPE_T0
+        mb_wait(F(b), (unsigned)(i >> 1) & 1u);
+        PIPE_ACC(0)
+      }
+      const long long k = kb[b];
+      if (k < 0) break;
+      {
+        PIPE_T0
+        solve_one<N, false, false, PH_G>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+        PIPE_ACC(1)
+      }
+      mb_arrive(D(b));
+    }
+  } else {  // front/tail team
+    const Team T{(int)threadIdx.x - kPipeGT, kPipeLT, w - CFB_PIPE_GW, 2};
+    int nprod = 0, stop = INT_MAX;
+    auto produce = [&]() {
+      const int j = nprod++, b = j & 1;
+      if (T.t == 0) {
+        const unsigned long long c = atomicAdd(a.claim, 1ull);
+        kb[b] = c < (unsigned long long)a.n_inst ? (long long)c : -1;
+      }
+      T.sync();
+      const long long k = kb[b];
+      if (k >= 0) solve_one<N, false, false, PH_FRONT>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+      else stop = j;
+      mb_arrive(F(b));
+    };
+    // fills j = 0, 1, 2, ... go to buffer j & 1; the tail of fill i runs
+    // before fill i + 2 (one call site each: the phases are large)
+    for (int step = 0;; ++step) {
+      if (step >= 2) {
+        const int i = step - 2, b = i & 1;
+        if (i >= stop) break;
+        {
+          PIPE_T0
+          mb_wait(D(b), (unsigned)(i >> 1) & 1u);
+          PIPE_ACC(2)
+        }
+        PIPE_T0
+        const long long k = kb[b];
+        solve_one<N, false, false, PH_TAIL>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+        PIPE_ACC(3)
+      }
+      if (stop == INT_MAX) produce();
+    }
+  }
+}
+
 int fixed_smem_bytes(int M, int N) { return 8 * M * rec_size(N) + 8 * M + 4 * M + 16; }
 
 // ------------------------------------------------------------ host launch
@@ -217,6 +362,40 @@ extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {
 
 cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t st) {
 #define CFB_CALL(n) return launch_small_n<n>(a, threads, grid, st)
+  CFB_DISPATCH_N(a.P.N, CFB_CALL)
+#undef CFB_CALL
+}
+
+
+bool pipe_fits(int M, int N) { return M >= 1 && 2 * pipe_buf_bytes(M, N) + 64 <= 227 * 1024; }
+
+template <int N>
+static cudaError_t launch_pipe_n(const SmallArgs& a_in, cudaStream_t st) {
+  SmallArgs a = a_in;
+  a.L = make_layout(a.M, N, 4);
+  const int smem = 2 * pipe_buf_bytes(a.M, N);
+  if (!pipe_fits(a.M, N) || !a.claim) return cudaErrorInvalidValue;
+  cudaError_t e = ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
+  if (e != cudaSuccess) return e;
+  static thread_local int last_smem = -1, per_sm = 1, sms = 148;
+  if (smem != last_smem) {  // occupancy of this buffer size
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pipe_kernel<N>, kPipeT, smem);
+    if (per_sm < 1) per_sm = 1;
+    last_smem = smem;
+  }
+  const long long want = (a.n_inst + 1) / 2;  // two instances in flight per CTA
+  const int grid = (int)(want < (long long)per_sm * sms ? want : (long long)per_sm * sms);
+  e = cudaMemsetAsync(a.claim, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  solve_pipe_kernel<N><<<grid, kPipeT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pipe(const SmallArgs& a, cudaStream_t st) {
+#define CFB_CALL(n) return launch_pipe_n<n>(a, st)
   CFB_DISPATCH_N(a.P.N, CFB_CALL)
 #undef CFB_CALL
 }

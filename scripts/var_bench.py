@@ -15,7 +15,8 @@ import numpy as np, torch
 import checkers as ck
 from paper_2206_06304_b200 import Engine, profile_heavy, profile_light, sample_batch, sub_seed
 eng = Engine(0)
-for M, K, light in [(50, 1024, False), (20, 512, False), (14, 256, True), (100, 64, False), (7, 256, False), (33, 256, True)]:
+NOCHECK = bool(os.environ.get("VB_NOCHECK"))  # timing-only experiment builds (CFB_EXP_*)
+for M, K, light in ([] if NOCHECK else [(50, 1024, False), (20, 512, False), (14, 256, True), (100, 64, False), (7, 256, False), (33, 256, True), (50, 4096, False), (20, 4096, True), (64, 4096, False), (1, 4096, False), (3, 3000, True)]):
     prof = profile_light(M) if light else profile_heavy(M)
     u = sample_batch(K, M, prof, 0.05 if light else 0.25, 0.2 if light else 1.0, seed=M + 1000)
     ip, og = eng.sweep(prof, u)
@@ -32,15 +33,16 @@ chk = {k: v[:2000].cpu().numpy() for k, v in dev.items()}
 ip, og = eng.sweep(prof, dev)
 ipc = {k: v[:2000].cpu().numpy() for k, v in ip.items()}
 ogc = {k: v[:2000].cpu().numpy() for k, v in og.items()}
-ck.assert_same_ip(ipc, ck.oracle_ipssa(prof, chk), where="C3 head")
-ck.assert_same_og(ogc, ck.oracle_og(prof, chk), where="C3 head")
+if not NOCHECK:
+    ck.assert_same_ip(ipc, ck.oracle_ipssa(prof, chk), where="C3 head")
+    ck.assert_same_og(ogc, ck.oracle_og(prof, chk), where="C3 head")
 ts = []
 for rep in range(5):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(); eng.sweep(prof, dev); e.record(); torch.cuda.synchronize()
     ts.append(s.elapsed_time(e))
-print(f"RESULT {os.path.basename(os.environ['COINFER_LIB'])}: parity ok; C3 sweep K={K}: best {min(ts):.2f} ms "
+print(f"RESULT {os.path.basename(os.environ['COINFER_LIB'])}: {'unchecked' if NOCHECK else 'parity ok'}; C3 sweep K={K}: best {min(ts):.2f} ms "
       f"median {sorted(ts)[2]:.2f} ms -> {K / min(ts) * 1e3 / 1e6:.3f} M inst/s")
 '''.replace("ROOT", repr(ROOT))
 
