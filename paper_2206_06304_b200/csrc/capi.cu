@@ -55,6 +55,10 @@ struct coinfer_ctx {
   static constexpr int kClaims = 64;
   unsigned long long* claim = nullptr;
   int claim_next = 0;
+  // pipelined kernel: global G tables, one workspace per stream it runs on
+  // (ctx->stream, pipe[0], pipe[1]: launches on different streams may overlap)
+  double* gg[3] = {nullptr, nullptr, nullptr};
+  size_t gg_cap[3] = {0, 0, 0};
 };
 
 namespace cfb {
@@ -462,6 +466,20 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
       }
       cfb::SmallArgs ap = args;
       ap.claim = ctx->claim + (ctx->claim_next++ % coinfer_ctx::kClaims);
+      {  // its G tables live in global memory (L2)
+        const int gs = st == ctx->pipe[1] ? 2 : st == ctx->pipe[0] ? 1 : 0;
+        const size_t need = cfb::pipe_gg_doubles((int)M, (int)N);
+        if (need > ctx->gg_cap[gs]) {
+          cudaStreamSynchronize(st);
+          if (ctx->gg[gs]) cudaFree(ctx->gg[gs]);
+          ctx->gg[gs] = nullptr;
+          ctx->gg_cap[gs] = 0;
+          cudaError_t e = cudaMalloc(&ctx->gg[gs], need * sizeof(double));
+          if (e != cudaSuccess) return e;
+          ctx->gg_cap[gs] = need;
+        }
+        ap.gg = ctx->gg[gs];
+      }
       return cfb::launch_pipe(ap, st);
     }
     static const int wide = std::getenv("COINFER_WIDE") ? std::atoi(std::getenv("COINFER_WIDE")) : 512;
@@ -912,6 +930,8 @@ void coinfer_ctx_destroy(coinfer_ctx* ctx) {
   if (ctx->lstart) cudaEventDestroy(ctx->lstart);
   if (ctx->aux) cudaFree(ctx->aux);
   if (ctx->claim) cudaFree(ctx->claim);
+  for (int i = 0; i < 3; ++i)
+    if (ctx->gg[i]) cudaFree(ctx->gg[i]);
   for (int i = 0; i < 2; ++i) {
     if (ctx->pipe[i]) cudaStreamSynchronize(ctx->pipe[i]);
     if (ctx->ws2[i]) cudaFree(ctx->ws2[i]);

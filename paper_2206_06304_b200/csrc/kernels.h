@@ -37,6 +37,8 @@ struct SmallArgs {
   unsigned long long* ctr;
   // instance claim counter of the pipelined kernel (zeroed before each launch)
   unsigned long long* claim;
+  // pipelined kernel: G tables in global memory, 2 per CTA (pipe_gg_doubles), or NULL
+  double* gg;
 };
 enum { CTR_OG = 0, CTR_IP, CTR_LOCAL, CTR_BSTAR, CTR_STARTS, CTR_DP, CTR_INST, CTR_N = 8 };
 
@@ -166,6 +168,7 @@ cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t
 // this size do not fit (the caller then uses launch_small).
 cudaError_t launch_pipe(const SmallArgs& a, cudaStream_t st);
 bool pipe_fits(int M, int N);
+size_t pipe_gg_doubles(int M, int N);  // the global G-table workspace the pipelined kernel wants
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
 
 #ifdef CFB_ONLY_N  // development builds: one sub-task count only (fast compiles)

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(32) online_kernel(OnlineArgs o) {
         in.pd = nullptr;
         in.has_l_ip = false;  // IP-SSA at min deadline, as invoke_solver does
         in.l_ip = 0.0;
-        const Layout L = make_layout(ns, N, 1);
+        const Layout L = make_layout(ns, N);
         solve_one<N, true>(o.solve, e, obase, ns, in, sm, L);
         __syncthreads();
         if (tid == 0) {
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(32, CFB_ONLINE_WARP_MINB) online_warp_kernel(O
         in.pd = nullptr;
         in.has_l_ip = false;  // IP-SSA at min deadline, as invoke_solver does
         in.l_ip = 0.0;
-        const Layout L = make_layout(ns, N, 1);
+        const Layout L = make_layout(ns, N);
         solve_one<N, true>(o.solve, e, obase, ns, in, sm, L);
         __syncthreads();
         const bool og = o.solve.do_og;
@@ -711,19 +711,19 @@ extern "C" int coinfer_debug_online_phase_cycles(unsigned long long* out, int re
 #endif
 
 int online_warp_smem_bytes(int M, int N) {
-  const int solver = make_layout(M, N, 1).total;
+  const int solver = make_layout(M, N).total;
   return solver + 8 * 7 * M + 8 * 312 + 8 * 128 + 4 * 32 + 16;
 }
 
 int online_smem_bytes(int M, int N) {
-  const int solver = make_layout(M, N, 1).total;
+  const int solver = make_layout(M, N).total;
   return solver + 8 * (3 * M + 7 * M) + 8 * Mt64::n + 4 * (8 + M) + 16;
 }
 
 template <int N>
 static cudaError_t launch_online_n(const OnlineArgs& a_in, int grid, cudaStream_t st) {
   OnlineArgs a = a_in;
-  a.L = make_layout(a.M, N, 1);
+  a.L = make_layout(a.M, N);
   static const bool serial = std::getenv("COINFER_ONLINE_SERIAL") != nullptr;  // testing aid
   if (a.M <= 32 && !serial) {
     const int smem = online_warp_smem_bytes(a.M, N);

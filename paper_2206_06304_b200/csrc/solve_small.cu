@@ -197,6 +197,9 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
 #ifndef CFB_PIPE_LW
 #define CFB_PIPE_LW 2
 #endif
+#ifndef CFB_PIPE_LMAP
+#define CFB_PIPE_LMAP 0  // front/tail warps: 0 = the last ones, 1 = w % 4 == 3 (needs CFB_PIPE_LW = 2, 8 warps)
+#endif
 constexpr int kPipeGT = 32 * CFB_PIPE_GW, kPipeLT = 32 * CFB_PIPE_LW, kPipeT = kPipeGT + kPipeLT;
 
 __device__ __forceinline__ void mb_init(uint32_t addr, unsigned count) {
@@ -213,7 +216,7 @@ __device__ __forceinline__ void mb_wait(uint32_t addr, unsigned parity) {  // ac
       : : "r"(addr), "r"(parity) : "memory");
 }
 
-__host__ __device__ inline int pipe_buf_bytes(int M, int N) { return (make_layout(M, N, 4).total + 127) & ~127; }
+__host__ __device__ inline int pipe_buf_bytes(int M, int N) { return (make_layout(M, N, CFB_SLOT_PIPE).total + 127) & ~127; }
 
 #ifdef CFB_PIPE_PROF  // development: cycles each team spends waiting on the other
 static __device__ unsigned long long g_pipe_cyc[4];  // G wait, G busy, L wait, L busy (per warp-0 lane 0 of each team)
@@ -226,7 +229,7 @@ extern "C" int coinfer_debug_pipe_cycles(unsigned long long* out, int reset) {
   return 0;
 }
 #define PIPE_T0 const long long _t0 = clock64();
-#define PIPE_ACC(i) if ((threadIdx.x & 31) == 0 && (threadIdx.x == 0 || threadIdx.x == kPipeGT)) atomicAdd(&g_pipe_cyc[i], (unsigned long long)(clock64() - _t0));
+#define PIPE_ACC(i) if (T.t == 0) atomicAdd(&g_pipe_cyc[i], (unsigned long long)(clock64() - _t0));
 #else
 #define PIPE_T0
 #define PIPE_ACC(i)
@@ -243,6 +246,9 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(mbar);
   auto F = [&](int b) { return mb0 + 8u * (uint32_t)b; };
   auto D = [&](int b) { return mb0 + 16u + 8u * (uint32_t)b; };
+  // this CTA's two G tables in global memory (L2-resident)
+  const size_t gstride = ((size_t)M * (M + 1) / 2 + 31) & ~(size_t)31;
+  auto gbuf = [&](int b) { return a.gg + (2 * (size_t)blockIdx.x + b) * gstride; };
   if (threadIdx.x == 0) {
     mb_init(F(0), kPipeLT);
     mb_init(F(1), kPipeLT);
@@ -266,8 +272,16 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
     in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
     return in;
   };
-  if (w < CFB_PIPE_GW) {  // G team
-    const Team T{(int)threadIdx.x, kPipeGT, w, 1};
+  // Team roles by warp.  CFB_PIPE_LMAP 0: the last CFB_PIPE_LW warps run
+  // the front/tail; 1: warps 3, 7, ... (w % 4 == 3: the CTA's warps are
+  // spread over the SM's four sub-partitions by w % 4, so the front/tail
+  // warps of every CTA share one sub-partition and do not queue behind the
+  // issue-bound G warps on the other three).
+  const bool lteam = CFB_PIPE_LMAP ? (w & 3) == 3 : w >= CFB_PIPE_GW;
+  const int lw = CFB_PIPE_LMAP ? w >> 2 : w - CFB_PIPE_GW;      // rank among the front/tail warps
+  const int gw = CFB_PIPE_LMAP ? w - ((w + 1) >> 2) : w;        // rank among the G warps
+  if (!lteam) {  // G team
+    const Team T{gw * 32 + (int)(threadIdx.x & 31), kPipeGT, gw, 1};
     for (int i = 0;; ++i) {
       const int b = i & 1;
       {
@@ -279,13 +293,13 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
       if (k < 0) break;
       {
         PIPE_T0
-        solve_one<N, false, false, PH_G>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+        solve_one<N, false, false, PH_G>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
         PIPE_ACC(1)
       }
       mb_arrive(D(b));
     }
   } else {  // front/tail team
-    const Team T{(int)threadIdx.x - kPipeGT, kPipeLT, w - CFB_PIPE_GW, 2};
+    const Team T{lw * 32 + (int)(threadIdx.x & 31), kPipeLT, lw, 2};
     int nprod = 0, stop = INT_MAX;
     auto produce = [&]() {
       const int j = nprod++, b = j & 1;
@@ -295,7 +309,8 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
       }
       T.sync();
       const long long k = kb[b];
-      if (k >= 0) solve_one<N, false, false, PH_FRONT>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+      if (k >= 0)
+        solve_one<N, false, false, PH_FRONT>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
       else stop = j;
       mb_arrive(F(b));
     };
@@ -312,7 +327,7 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
         }
         PIPE_T0
         const long long k = kb[b];
-        solve_one<N, false, false, PH_TAIL>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T);
+        solve_one<N, false, false, PH_TAIL>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
         PIPE_ACC(3)
       }
       if (stop == INT_MAX) produce();
@@ -326,9 +341,8 @@ int fixed_smem_bytes(int M, int N) { return 8 * M * rec_size(N) + 8 * M + 4 * M 
 template <int N>
 static cudaError_t launch_small_n(const SmallArgs& a_in, int threads, int grid, cudaStream_t st) {
   if (a_in.ctr && threads > 256) threads = 256;  // the counting kernel is built for <= 256
-  const int W = threads / 32;
   SmallArgs a = a_in;
-  a.L = make_layout(a.M, N, W);
+  a.L = make_layout(a.M, N);
   const int smem = a.L.total;
   auto kern = a.ctr ? solve_count_kernel<N> : threads > 256 ? solve_wide_kernel<N> : solve_small_kernel<N>;
   cudaError_t e = ensure_smem((const void*)kern, smem, true);
@@ -369,25 +383,46 @@ cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t
 
 bool pipe_fits(int M, int N) { return M >= 1 && 2 * pipe_buf_bytes(M, N) + 64 <= 227 * 1024; }
 
+// CTAs of the pipelined kernel resident at once (its persistent grid)
 template <int N>
-static cudaError_t launch_pipe_n(const SmallArgs& a_in, cudaStream_t st) {
-  SmallArgs a = a_in;
-  a.L = make_layout(a.M, N, 4);
-  const int smem = 2 * pipe_buf_bytes(a.M, N);
-  if (!pipe_fits(a.M, N) || !a.claim) return cudaErrorInvalidValue;
-  cudaError_t e = ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
-  if (e != cudaSuccess) return e;
+static int pipe_max_grid(int M) {
+  const int smem = 2 * pipe_buf_bytes(M, N);
   static thread_local int last_smem = -1, per_sm = 1, sms = 148;
   if (smem != last_smem) {  // occupancy of this buffer size
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pipe_kernel<N>, kPipeT, smem);
     if (per_sm < 1) per_sm = 1;
     last_smem = smem;
   }
+  return per_sm * sms;
+}
+
+static cudaError_t pipe_grid_of(int M, int N, int* g) {
+#define CFB_CALL(n) *g = pipe_max_grid<n>(M); return cudaSuccess
+  CFB_DISPATCH_N(N, CFB_CALL)
+#undef CFB_CALL
+}
+
+size_t pipe_gg_doubles(int M, int N) {
+  int g = 0;
+  if (pipe_grid_of(M, N, &g) != cudaSuccess) return 0;
+  return (size_t)g * 2 * (((size_t)M * (M + 1) / 2 + 31) & ~(size_t)31);
+}
+
+template <int N>
+static cudaError_t launch_pipe_n(const SmallArgs& a_in, cudaStream_t st) {
+  SmallArgs a = a_in;
+  a.L = make_layout(a.M, N, CFB_SLOT_PIPE);
+  const int smem = 2 * pipe_buf_bytes(a.M, N);
+  if (!pipe_fits(a.M, N) || !a.claim || !a.gg) return cudaErrorInvalidValue;
+  cudaError_t e = ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
+  if (e != cudaSuccess) return e;
+  const long long maxg = pipe_max_grid<N>(a.M);
   const long long want = (a.n_inst + 1) / 2;  // two instances in flight per CTA
-  const int grid = (int)(want < (long long)per_sm * sms ? want : (long long)per_sm * sms);
+  const int grid = (int)(want < maxg ? want : maxg);
   e = cudaMemsetAsync(a.claim, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   solve_pipe_kernel<N><<<grid, kPipeT, smem, st>>>(a);
