@@ -197,6 +197,9 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
 #ifndef CFB_PIPE_LW
 #define CFB_PIPE_LW 2
 #endif
+#ifndef CFB_PIPE_SUSPEND_NS
+#define CFB_PIPE_SUSPEND_NS 1000000  // mbarrier wait suspend-time hint
+#endif
 #ifndef CFB_PIPE_LMAP
 #define CFB_PIPE_LMAP 0  // front/tail warps: 0 = the last ones, 1 = w % 4 == 3 (needs CFB_PIPE_LW = 2, 8 warps)
 #endif
@@ -208,12 +211,15 @@ __device__ __forceinline__ void mb_init(uint32_t addr, unsigned count) {
 __device__ __forceinline__ void mb_arrive(uint32_t addr) {  // release
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" : : "r"(addr) : "memory");
 }
-__device__ __forceinline__ void mb_wait(uint32_t addr, unsigned parity) {  // acquire
+// acquire; the thread is suspended in the hardware until the phase completes
+// (or the time hint runs out), instead of spinning on issue slots the
+// other warps need
+__device__ __forceinline__ void mb_wait(uint32_t addr, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}"
-      : : "r"(addr), "r"(parity) : "memory");
+      : : "r"(addr), "r"(parity), "r"(CFB_PIPE_SUSPEND_NS) : "memory");
 }
 
 __host__ __device__ inline int pipe_buf_bytes(int M, int N) { return (make_layout(M, N, CFB_SLOT_PIPE).total + 127) & ~127; }
@@ -239,6 +245,7 @@ template <int N>
 __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ long long kb[2];  // instance in buffer b, -1: none (stop)
+  __shared__ long long knext;  // the front/tail team's next claim
   __shared__ __align__(8) unsigned long long mbar[4];  // F[0], F[1], D[0], D[1]
   const int M = a.M;
   const int bufb = pipe_buf_bytes(M, N);
@@ -301,18 +308,36 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   } else {  // front/tail team
     const Team T{lw * 32 + (int)(threadIdx.x & 31), kPipeLT, lw, 2};
     int nprod = 0, stop = INT_MAX;
-    auto produce = [&]() {
-      const int j = nprod++, b = j & 1;
+    // The instance of the next fill is claimed one fill ahead and its inputs
+    // prefetched into L2, so the front does not wait on HBM.
+    auto claim = [&]() {
       if (T.t == 0) {
         const unsigned long long c = atomicAdd(a.claim, 1ull);
-        kb[b] = c < (unsigned long long)a.n_inst ? (long long)c : -1;
+        knext = c < (unsigned long long)a.n_inst ? (long long)c : -1;
       }
       T.sync();
-      const long long k = kb[b];
+      const long long kn = knext;
+      if (kn >= 0) {
+        const double* arrs[7] = {a.fmin, a.fmax, a.kappa, a.ru, a.pu, a.arr, a.dl};
+        const int lines = (M * 8 + 127) / 128 + 1;
+        for (int x = T.t; x < 7 * lines; x += T.nt) {
+          const int off = 128 * (x % lines) < 8 * (M - 1) ? 128 * (x % lines) : 8 * (M - 1);  // inside the instance
+          const char* p = reinterpret_cast<const char*>(arrs[x / lines] + (size_t)kn * M) + off;
+          asm volatile("prefetch.global.L2 [%0];" : : "l"(p));
+        }
+      }
+      return kn;
+    };
+    long long kpre = claim();
+    auto produce = [&]() {
+      const int j = nprod++, b = j & 1;
+      const long long k = kpre;
+      if (T.t == 0) kb[b] = k;
       if (k >= 0)
         solve_one<N, false, false, PH_FRONT>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
       else stop = j;
       mb_arrive(F(b));
+      if (k >= 0) kpre = claim();
     };
     // fills j = 0, 1, 2, ... go to buffer j & 1; the tail of fill i runs
     // before fill i + 2 (one call site each: the phases are large)
@@ -365,10 +390,12 @@ static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid
 extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
   cudaMemcpyFromSymbol(out + 8, g_ip_steps, sizeof(unsigned long long) * 2);
+  cudaMemcpyFromSymbol(out + 10, g_tail_cycles, sizeof(unsigned long long) * 4);
   if (reset) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     cudaMemcpyToSymbol(g_ip_steps, z, sizeof(unsigned long long) * 2);
+    cudaMemcpyToSymbol(g_tail_cycles, z, sizeof(unsigned long long) * 4);
   }
   return 0;
 }

@@ -10,12 +10,12 @@ eng = Engine(0)
 prof = profile_heavy(M)
 dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, M, prof, seed=1).items()}
 eng.sweep(prof, dev); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 10)()
+buf = (C.c_ulonglong * 14)()
 lib = _abi.load_library()
 lib.coinfer_debug_phase_cycles(buf, 1)
 eng.sweep(prof, dev); torch.cuda.synchronize()
 lib.coinfer_debug_phase_cycles(buf, 1)
-names = ["rows/pools/pfit", "G table", "IP-SSA out", "DP", "backtrack/b*/stitch", "check/sort/hoist"]
+names = ["rows/pools/pfit", "G table", "IP-SSA out", "DP", "group folds/final", "check/sort/hoist"]
 tot = sum(buf[:6])
 for i in [5, 0, 1, 2, 3, 4]:
     print(f"{names[i]:24s} {buf[i]/K:12.0f} cycles/instance  {buf[i]/tot*100:5.1f}%")
@@ -25,3 +25,7 @@ if buf[7]:
 if buf[9]:
     print(f"IP-SSA G loop: {buf[8]/K:.0f} active lane-steps/instance, {buf[9]/K:.0f} warp-steps/instance, "
           f"lane utilisation {buf[8]/(32*buf[9])*100:.1f}%")
+tn = ["best_i/order", "backtrack/gid", "gitem/b*/gbest", "stitch"]
+if any(buf[10:14]):
+    for i in range(4):
+        print(f"  tail {tn[i]:20s} {buf[10 + i]/K:10.0f} cycles/instance")
