@@ -245,7 +245,6 @@ template <int N>
 __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ long long kb[2];  // instance in buffer b, -1: none (stop)
-  __shared__ long long knext;  // the front/tail team's next claim
   __shared__ __align__(8) unsigned long long mbar[4];  // F[0], F[1], D[0], D[1]
   const int M = a.M;
   const int bufb = pipe_buf_bytes(M, N);
@@ -308,36 +307,18 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   } else {  // front/tail team
     const Team T{lw * 32 + (int)(threadIdx.x & 31), kPipeLT, lw, 2};
     int nprod = 0, stop = INT_MAX;
-    // The instance of the next fill is claimed one fill ahead and its inputs
-    // prefetched into L2, so the front does not wait on HBM.
-    auto claim = [&]() {
-      if (T.t == 0) {
-        const unsigned long long c = atomicAdd(a.claim, 1ull);
-        knext = c < (unsigned long long)a.n_inst ? (long long)c : -1;
-      }
-      T.sync();
-      const long long kn = knext;
-      if (kn >= 0) {
-        const double* arrs[7] = {a.fmin, a.fmax, a.kappa, a.ru, a.pu, a.arr, a.dl};
-        const int lines = (M * 8 + 127) / 128 + 1;
-        for (int x = T.t; x < 7 * lines; x += T.nt) {
-          const int off = 128 * (x % lines) < 8 * (M - 1) ? 128 * (x % lines) : 8 * (M - 1);  // inside the instance
-          const char* p = reinterpret_cast<const char*>(arrs[x / lines] + (size_t)kn * M) + off;
-          asm volatile("prefetch.global.L2 [%0];" : : "l"(p));
-        }
-      }
-      return kn;
-    };
-    long long kpre = claim();
     auto produce = [&]() {
       const int j = nprod++, b = j & 1;
-      const long long k = kpre;
-      if (T.t == 0) kb[b] = k;
+      if (T.t == 0) {
+        const unsigned long long c = atomicAdd(a.claim, 1ull);
+        kb[b] = c < (unsigned long long)a.n_inst ? (long long)c : -1;
+      }
+      T.sync();
+      const long long k = kb[b];
       if (k >= 0)
         solve_one<N, false, false, PH_FRONT>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
       else stop = j;
       mb_arrive(F(b));
-      if (k >= 0) kpre = claim();
     };
     // fills j = 0, 1, 2, ... go to buffer j & 1; the tail of fill i runs
     // before fill i + 2 (one call site each: the phases are large)
