@@ -14,6 +14,14 @@ for M, K, lo, hi in [(50, 64, 0.25, 1.0), (20, 32, 0.5, 3.0), (100, 4, 0.25, 1.0
     ip, og = eng.sweep(prof, u)
     ck.assert_same_ip(ip, ck.oracle_ipssa(prof, u)); ck.assert_same_og(og, ck.oracle_og(prof, u))
     print("small path ok", M, K, flush=True)
+# the pipelined persistent kernel (K >= 2048, M <= 64): teams, named barriers,
+# mbarriers, the L2 G tables
+for M, K, lo, hi, light in [(50, 2100, 0.25, 1.0, False), (20, 2048, 0.05, 0.2, True), (64, 2048, 0.25, 1.0, False)]:
+    prof = profile_light(M) if light else profile_heavy(M)
+    u = sample_batch(K, M, prof, lo, hi, seed=M + 7)
+    ip, og = eng.sweep(prof, u)
+    ck.assert_same_ip(ip, ck.oracle_ipssa(prof, u)); ck.assert_same_og(og, ck.oracle_og(prof, u))
+    print("pipelined path ok", M, K, flush=True)
 for M, lo, hi in [(300, 0.5, 3.0), (260, 0.25, 1.0)]:
     prof = profile_heavy(M)
     u = sample_batch(1, M, prof, lo, hi, seed=M)
