@@ -456,9 +456,9 @@ int run(coinfer_ctx* ctx, const coinfer_profile* prof, const coinfer_users* user
     // Many small instances: the pipelined kernel (two instances per CTA,
     // G-phase warps apart from front/tail warps) when two buffers fit.
     static const char* pipe_env = std::getenv("COINFER_PIPE");
-    static const int pipe_maxm = std::getenv("COINFER_PIPE_MAXM") ? std::atoi(std::getenv("COINFER_PIPE_MAXM"))
-                                                                   : CFB_PIPE_MAXM;
-    if (!args.ctr && Kc >= 2048 && (int)M <= pipe_maxm && cfb::pipe_fits((int)M, (int)N) &&
+    const bool pipe_force = pipe_env && pipe_env[0] == '1';  // testing aid: whenever it fits
+    if (!args.ctr && Kc >= 2048 &&
+        (pipe_force ? cfb::pipe_fits((int)M, (int)N) : cfb::pipe_preferred((int)M, (int)N)) &&
         !(pipe_env && pipe_env[0] == '0')) {
       if (!ctx->claim) {
         cudaError_t e = cudaMalloc(&ctx->claim, sizeof(unsigned long long) * coinfer_ctx::kClaims);

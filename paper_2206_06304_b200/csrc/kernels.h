@@ -168,6 +168,9 @@ cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t
 // this size do not fit (the caller then uses launch_small).
 cudaError_t launch_pipe(const SmallArgs& a, cudaStream_t st);
 bool pipe_fits(int M, int N);
+// Whether the pipelined kernel beats the one-CTA kernel at this size (by
+// the instances each keeps in flight per SM; measured crossovers, see there)
+bool pipe_preferred(int M, int N);
 size_t pipe_gg_doubles(int M, int N);  // the global G-table workspace the pipelined kernel wants
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
 

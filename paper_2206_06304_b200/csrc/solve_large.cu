@@ -442,8 +442,10 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
           pma[c] = r < q1c ? 0 : colA[r];
           const int slot = j & (DR - 1), qj = q1[j];
           qjv[c] = qj;
-          pmj[c] = i == qj ? S0[j] : runV[slot];
-          paj[c] = i == qj ? 0 : runA[slot];
+          // (clamped lanes past the row read nothing: another lane owns slot M-1)
+          const bool own = i + 32 * c + lane < M;
+          pmj[c] = !own ? INF : i == qj ? S0[j] : runV[slot];
+          paj[c] = !own ? 0 : i == qj ? 0 : runA[slot];
         }
         double best[3];
         int bp[3];

@@ -203,7 +203,29 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
 #ifndef CFB_PIPE_LMAP
 #define CFB_PIPE_LMAP 0  // front/tail warps: 0 = the last ones, 1 = w % 4 == 3 (needs CFB_PIPE_LW = 2, 8 warps)
 #endif
-constexpr int kPipeGT = 32 * CFB_PIPE_GW, kPipeLT = 32 * CFB_PIPE_LW, kPipeT = kPipeGT + kPipeLT;
+#ifndef CFB_PIPE_GW1
+#define CFB_PIPE_GW1 20  // the same for 64 < M <= 128: one CTA of 24 warps per SM
+#endif
+#ifndef CFB_PIPE_LW1
+#define CFB_PIPE_LW1 4
+#endif
+#ifndef CFB_PIPE_GW2
+#define CFB_PIPE_GW2 12  // ... when two CTAs of two buffers fit an SM
+#endif
+#ifndef CFB_PIPE_LW2
+#define CFB_PIPE_LW2 4
+#endif
+// Team shapes by how many CTAs (two instance buffers each) fit an SM's
+// shared memory: 0 = four (8 warps each), 2 = two (16), 1 = one (24);
+// 64 registers per thread in every case.
+template <int S>
+struct PipeShape {
+  static constexpr int GW = S == 0 ? CFB_PIPE_GW : S == 1 ? CFB_PIPE_GW1 : CFB_PIPE_GW2;
+  static constexpr int LW = S == 0 ? CFB_PIPE_LW : S == 1 ? CFB_PIPE_LW1 : CFB_PIPE_LW2;
+  static constexpr int GT = 32 * GW, LT = 32 * LW, T = GT + LT;
+  static constexpr int MINB = S == 0 ? 4 : S == 2 ? 2 : 1;
+  static constexpr bool LMAP = S == 0 && CFB_PIPE_LMAP;
+};
 
 __device__ __forceinline__ void mb_init(uint32_t addr, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" : : "r"(addr), "r"(count) : "memory");
@@ -241,8 +263,10 @@ extern "C" int coinfer_debug_pipe_cycles(unsigned long long* out, int reset) {
 #define PIPE_ACC(i)
 #endif
 
-template <int N>
-__global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
+template <int N, int S>
+__global__ void __launch_bounds__(PipeShape<S>::T, PipeShape<S>::MINB) solve_pipe_kernel(SmallArgs a) {
+  using PS = PipeShape<S>;
+  constexpr int kPipeGT = PS::GT, kPipeLT = PS::LT, CFB_PIPE_GW_ = PS::GW;
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ long long kb[2];  // instance in buffer b, -1: none (stop)
   __shared__ __align__(8) unsigned long long mbar[4];  // F[0], F[1], D[0], D[1]
@@ -283,9 +307,9 @@ __global__ void __launch_bounds__(kPipeT, 4) solve_pipe_kernel(SmallArgs a) {
   // spread over the SM's four sub-partitions by w % 4, so the front/tail
   // warps of every CTA share one sub-partition and do not queue behind the
   // issue-bound G warps on the other three).
-  const bool lteam = CFB_PIPE_LMAP ? (w & 3) == 3 : w >= CFB_PIPE_GW;
-  const int lw = CFB_PIPE_LMAP ? w >> 2 : w - CFB_PIPE_GW;      // rank among the front/tail warps
-  const int gw = CFB_PIPE_LMAP ? w - ((w + 1) >> 2) : w;        // rank among the G warps
+  const bool lteam = PS::LMAP ? (w & 3) == 3 : w >= CFB_PIPE_GW_;
+  const int lw = PS::LMAP ? w >> 2 : w - CFB_PIPE_GW_;      // rank among the front/tail warps
+  const int gw = PS::LMAP ? w - ((w + 1) >> 2) : w;         // rank among the G warps
   if (!lteam) {  // G team
     const Team T{gw * 32 + (int)(threadIdx.x & 31), kPipeGT, gw, 1};
     for (int i = 0;; ++i) {
@@ -371,12 +395,12 @@ static cudaError_t launch_fixed_n(const SmallArgs& a, const int32_t* b, int grid
 extern "C" int coinfer_debug_phase_cycles(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
   cudaMemcpyFromSymbol(out + 8, g_ip_steps, sizeof(unsigned long long) * 2);
-  cudaMemcpyFromSymbol(out + 10, g_tail_cycles, sizeof(unsigned long long) * 4);
+  cudaMemcpyFromSymbol(out + 10, g_tail_cycles, sizeof(unsigned long long) * 8);
   if (reset) {
     unsigned long long z[8] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
     cudaMemcpyToSymbol(g_ip_steps, z, sizeof(unsigned long long) * 2);
-    cudaMemcpyToSymbol(g_tail_cycles, z, sizeof(unsigned long long) * 4);
+    cudaMemcpyToSymbol(g_tail_cycles, z, sizeof(unsigned long long) * 8);
   }
   return 0;
 }
@@ -390,9 +414,25 @@ cudaError_t launch_small(const SmallArgs& a, int threads, int grid, cudaStream_t
 
 
 bool pipe_fits(int M, int N) { return M >= 1 && 2 * pipe_buf_bytes(M, N) + 64 <= 227 * 1024; }
+static int pipe_shape(int M, int N) {
+  const int cta = 2 * pipe_buf_bytes(M, N) + 64 + 1024;  // + the per-CTA reservation
+  return 4 * cta <= 228 * 1024 ? 0 : 2 * cta <= 228 * 1024 ? 2 : 1;
+}
+// Measured at N = 4, 100k instances (pipelined vs one-CTA, ms): M = 40
+// 7.6 / 8.3, 50 91.5 / 111.6 (1M), 56 15.4 / 14.5, 64 17.6 / 19.0, 72
+// 20.4 / 25.6, 80 35.2 / 29.4, 90 39.8 / 42.6, 100 45.1 / 49.4.
+bool pipe_preferred(int M, int N) {
+  if (!pipe_fits(M, N)) return false;
+  const int sh = pipe_shape(M, N);
+  if (sh == 0) return true;
+  if (sh == 1) return M >= 88;  // one CTA per SM: only past the measured crossover
+  const int one = make_layout(M, N).total + 1024;  // one-CTA kernel: instances per SM by shared memory
+  const int small_inst = (228 * 1024) / one;
+  return 4 >= small_inst - 1;
+}
 
 // CTAs of the pipelined kernel resident at once (its persistent grid)
-template <int N>
+template <int N, int S>
 static int pipe_max_grid(int M) {
   const int smem = 2 * pipe_buf_bytes(M, N);
   static thread_local int last_smem = -1, per_sm = 1, sms = 148;
@@ -400,16 +440,22 @@ static int pipe_max_grid(int M) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pipe_kernel<N>, kPipeT, smem);
+    ensure_smem((const void*)solve_pipe_kernel<N, S>, smem, true);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_pipe_kernel<N, S>, PipeShape<S>::T, smem);
     if (per_sm < 1) per_sm = 1;
     last_smem = smem;
   }
   return per_sm * sms;
 }
 
+template <int N>
+static int pipe_max_grid_m(int M) {
+  const int sh = pipe_shape(M, N);
+  return sh == 0 ? pipe_max_grid<N, 0>(M) : sh == 2 ? pipe_max_grid<N, 2>(M) : pipe_max_grid<N, 1>(M);
+}
+
 static cudaError_t pipe_grid_of(int M, int N, int* g) {
-#define CFB_CALL(n) *g = pipe_max_grid<n>(M); return cudaSuccess
+#define CFB_CALL(n) *g = pipe_max_grid_m<n>(M); return cudaSuccess
   CFB_DISPATCH_N(N, CFB_CALL)
 #undef CFB_CALL
 }
@@ -420,21 +466,27 @@ size_t pipe_gg_doubles(int M, int N) {
   return (size_t)g * 2 * (((size_t)M * (M + 1) / 2 + 31) & ~(size_t)31);
 }
 
-template <int N>
-static cudaError_t launch_pipe_n(const SmallArgs& a_in, cudaStream_t st) {
+template <int N, int S>
+static cudaError_t launch_pipe_ns(const SmallArgs& a_in, cudaStream_t st) {
   SmallArgs a = a_in;
   a.L = make_layout(a.M, N, CFB_SLOT_PIPE);
   const int smem = 2 * pipe_buf_bytes(a.M, N);
   if (!pipe_fits(a.M, N) || !a.claim || !a.gg) return cudaErrorInvalidValue;
-  cudaError_t e = ensure_smem((const void*)solve_pipe_kernel<N>, smem, true);
+  cudaError_t e = ensure_smem((const void*)solve_pipe_kernel<N, S>, smem, true);
   if (e != cudaSuccess) return e;
-  const long long maxg = pipe_max_grid<N>(a.M);
+  const long long maxg = pipe_max_grid<N, S>(a.M);
   const long long want = (a.n_inst + 1) / 2;  // two instances in flight per CTA
   const int grid = (int)(want < maxg ? want : maxg);
   e = cudaMemsetAsync(a.claim, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  solve_pipe_kernel<N><<<grid, kPipeT, smem, st>>>(a);
+  solve_pipe_kernel<N, S><<<grid, PipeShape<S>::T, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_pipe_n(const SmallArgs& a, cudaStream_t st) {
+  const int sh = pipe_shape(a.M, N);
+  return sh == 0 ? launch_pipe_ns<N, 0>(a, st) : sh == 2 ? launch_pipe_ns<N, 2>(a, st) : launch_pipe_ns<N, 1>(a, st);
 }
 
 cudaError_t launch_pipe(const SmallArgs& a, cudaStream_t st) {

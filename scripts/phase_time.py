@@ -10,7 +10,7 @@ eng = Engine(0)
 prof = profile_heavy(M)
 dev = {k: torch.as_tensor(v, device="cuda") for k, v in sample_batch(K, M, prof, seed=1).items()}
 eng.sweep(prof, dev); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 14)()
+buf = (C.c_ulonglong * 18)()
 lib = _abi.load_library()
 lib.coinfer_debug_phase_cycles(buf, 1)
 eng.sweep(prof, dev); torch.cuda.synchronize()
@@ -25,7 +25,7 @@ if buf[7]:
 if buf[9]:
     print(f"IP-SSA G loop: {buf[8]/K:.0f} active lane-steps/instance, {buf[9]/K:.0f} warp-steps/instance, "
           f"lane utilisation {buf[8]/(32*buf[9])*100:.1f}%")
-tn = ["best_i/order", "backtrack/gid", "gitem/b*/gbest", "stitch"]
-if any(buf[10:14]):
-    for i in range(4):
+tn = ["best_i/order", "backtrack/gid", "gitem/b*/gbest", "stitch", "front: check", "front: rank/rec/lat", "front: b0/rlen/init"]
+if any(buf[10:17]):
+    for i in range(7):
         print(f"  tail {tn[i]:20s} {buf[10 + i]/K:10.0f} cycles/instance")

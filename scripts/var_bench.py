@@ -16,7 +16,7 @@ import checkers as ck
 from paper_2206_06304_b200 import Engine, profile_heavy, profile_light, sample_batch, sub_seed
 eng = Engine(0)
 NOCHECK = bool(os.environ.get("VB_NOCHECK"))  # timing-only experiment builds (CFB_EXP_*)
-for M, K, light in ([] if NOCHECK else [(50, 1024, False), (20, 512, False), (14, 256, True), (100, 64, False), (7, 256, False), (33, 256, True), (50, 4096, False), (20, 4096, True), (64, 4096, False), (1, 4096, False), (3, 3000, True)]):
+for M, K, light in ([] if NOCHECK else [(50, 1024, False), (20, 512, False), (14, 256, True), (100, 64, False), (7, 256, False), (33, 256, True), (50, 4096, False), (20, 4096, True), (64, 4096, False), (1, 4096, False), (3, 3000, True), (100, 2048, False), (90, 2100, True)]):
     prof = profile_light(M) if light else profile_heavy(M)
     u = sample_batch(K, M, prof, 0.05 if light else 0.25, 0.2 if light else 1.0, seed=M + 1000)
     ip, og = eng.sweep(prof, u)

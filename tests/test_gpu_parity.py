@@ -151,6 +151,22 @@ def test_heavy_profile_C3_sample(engine):
     check_sweep(engine, prof, users)
 
 
+@pytest.mark.parametrize("M,K,light", [(40, 2048, False), (64, 2048, False), (72, 2048, True), (100, 2048, False)])
+def test_pipelined_kernel_shapes(engine, M, K, light):
+    """Batches of >= 2048 instances run the pipelined kernel (solve_pipe_kernel)
+    in each of its team shapes: four CTAs per SM (M = 40), two (64, 72), one
+    (100).  Every instance against the oracle for M <= 72; at M = 100 the
+    first 256 and the last 64 (the oracle's O(M^3 N) cost)."""
+    prof = profile_light(M) if light else profile_heavy(M)
+    users = sample_batch(K, M, prof, 0.05 if light else 0.25, 0.2 if light else 1.0, seed=M + 3)
+    ip, og = engine.sweep(prof, users)
+    parts = [(0, K)] if M <= 72 else [(0, 256), (K - 64, K)]
+    for k0, k1 in parts:
+        sub = ck.slice_users(users, k0, k1)
+        ck.assert_same_ip({k: v[k0:k1] for k, v in ip.items()}, ck.oracle_ipssa(prof, sub), where=f"M={M} [{k0},{k1})")
+        ck.assert_same_og({k: v[k0:k1] for k, v in og.items()}, ck.oracle_og(prof, sub), where=f"M={M} [{k0},{k1})")
+
+
 def test_light_profile_online_shape(engine):
     prof = profile_light(14)
     users = sample_batch(512, 14, prof, 0.05, 0.2, seed=12)
