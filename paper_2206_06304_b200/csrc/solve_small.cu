@@ -204,16 +204,16 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
 #define CFB_PIPE_LMAP 0  // front/tail warps: 0 = the last ones, 1 = w % 4 == 3 (needs CFB_PIPE_LW = 2, 8 warps)
 #endif
 #ifndef CFB_PIPE_GW1
-#define CFB_PIPE_GW1 20  // the same for 64 < M <= 128: one CTA of 24 warps per SM
-#endif
+#define CFB_PIPE_GW1 16  // when one CTA of two buffers fits an SM: 24 warps (M=100 target,
+#endif                   // 100k instances: 20+4 / 18+6 / 16+8 / 14+10 -> 45.1 / 43.3 / 42.6 / 42.3 ms)
 #ifndef CFB_PIPE_LW1
-#define CFB_PIPE_LW1 4
+#define CFB_PIPE_LW1 8
 #endif
 #ifndef CFB_PIPE_GW2
-#define CFB_PIPE_GW2 12  // ... when two CTAs of two buffers fit an SM
+#define CFB_PIPE_GW2 10  // ... when two fit: 16 warps (M=64: 12+4 / 11+5 / 10+6 -> 17.3 / 17.1 / 16.9 ms)
 #endif
 #ifndef CFB_PIPE_LW2
-#define CFB_PIPE_LW2 4
+#define CFB_PIPE_LW2 6
 #endif
 // Team shapes by how many CTAs (two instance buffers each) fit an SM's
 // shared memory: 0 = four (8 warps each), 2 = two (16), 1 = one (24);
@@ -419,8 +419,8 @@ static int pipe_shape(int M, int N) {
   return 4 * cta <= 228 * 1024 ? 0 : 2 * cta <= 228 * 1024 ? 2 : 1;
 }
 // Measured at N = 4, 100k instances (pipelined vs one-CTA, ms): M = 40
-// 7.6 / 8.3, 50 91.5 / 111.6 (1M), 56 15.4 / 14.5, 64 17.6 / 19.0, 72
-// 20.4 / 25.6, 80 35.2 / 29.4, 90 39.8 / 42.6, 100 45.1 / 49.4.
+// 7.6 / 8.3, 50 90.6 / 111.6 (1M), 56 14.8 / 14.5, 64 16.9 / 19.0, 72
+// 19.7 / 25.6, 80 35.2 / 29.4, 90 37.7 / 42.6, 100 42.6 / 49.4.
 bool pipe_preferred(int M, int N) {
   if (!pipe_fits(M, N)) return false;
   const int sh = pipe_shape(M, N);
