@@ -420,12 +420,13 @@ static int pipe_shape(int M, int N) {
 }
 // Measured at N = 4, 100k instances (pipelined vs one-CTA, ms): M = 40
 // 7.6 / 8.3, 50 90.6 / 111.6 (1M), 56 14.8 / 14.5, 64 16.9 / 19.0, 72
-// 19.7 / 25.6, 80 35.2 / 29.4, 90 37.7 / 42.6, 100 42.6 / 49.4.
+// 19.7 / 25.6, 80 33.2 / 29.8, 84 35.1 / 40.1, 88 36.9 / 42.1, 90 37.7 /
+// 42.6, 100 42.6 / 49.4.
 bool pipe_preferred(int M, int N) {
   if (!pipe_fits(M, N)) return false;
   const int sh = pipe_shape(M, N);
   if (sh == 0) return true;
-  if (sh == 1) return M >= 88;  // one CTA per SM: only past the measured crossover
+  if (sh == 1) return M >= 82;  // one CTA per SM: only past the measured crossover (80 -> 84)
   const int one = make_layout(M, N).total + 1024;  // one-CTA kernel: instances per SM by shared memory
   const int small_inst = (228 * 1024) / one;
   return 4 >= small_inst - 1;
