@@ -200,9 +200,6 @@ __global__ void __launch_bounds__(128) fixed_batch_kernel(SmallArgs a, const int
 #ifndef CFB_PIPE_SUSPEND_NS
 #define CFB_PIPE_SUSPEND_NS 1000000  // mbarrier wait suspend-time hint
 #endif
-#ifndef CFB_PIPE_LMAP
-#define CFB_PIPE_LMAP 0  // front/tail warps: 0 = the last ones, 1 = w % 4 == 3 (needs CFB_PIPE_LW = 2, 8 warps)
-#endif
 #ifndef CFB_PIPE_GW1
 #define CFB_PIPE_GW1 16  // when one CTA of two buffers fits an SM: 24 warps (M=100 target,
 #endif                   // 100k instances: 20+4 / 18+6 / 16+8 / 14+10 -> 45.1 / 43.3 / 42.6 / 42.3 ms)
@@ -224,7 +221,6 @@ struct PipeShape {
   static constexpr int LW = S == 0 ? CFB_PIPE_LW : S == 1 ? CFB_PIPE_LW1 : CFB_PIPE_LW2;
   static constexpr int GT = 32 * GW, LT = 32 * LW, T = GT + LT;
   static constexpr int MINB = S == 0 ? 4 : S == 2 ? 2 : 1;
-  static constexpr bool LMAP = S == 0 && CFB_PIPE_LMAP;
 };
 
 __device__ __forceinline__ void mb_init(uint32_t addr, unsigned count) {
@@ -302,14 +298,15 @@ __global__ void __launch_bounds__(PipeShape<S>::T, PipeShape<S>::MINB) solve_pip
     in.l_ip = a.l_ip ? a.l_ip[k] : 0.0;
     return in;
   };
-  // Team roles by warp.  CFB_PIPE_LMAP 0: the last CFB_PIPE_LW warps run
-  // the front/tail; 1: warps 3, 7, ... (w % 4 == 3: the CTA's warps are
-  // spread over the SM's four sub-partitions by w % 4, so the front/tail
-  // warps of every CTA share one sub-partition and do not queue behind the
-  // issue-bound G warps on the other three).
-  const bool lteam = PS::LMAP ? (w & 3) == 3 : w >= CFB_PIPE_GW_;
-  const int lw = PS::LMAP ? w >> 2 : w - CFB_PIPE_GW_;      // rank among the front/tail warps
-  const int gw = PS::LMAP ? w - ((w + 1) >> 2) : w;         // rank among the G warps
+  // Team roles by warp: the last warps run the front/tail.  (The SM places
+  // warp w of its c-th resident CTA on sub-partition (w + c) % 4, measured
+  // with %warpid, so each sub-partition hosts two front/tail warps and six
+  // G warps.  Putting all front/tail warps on one sub-partition cut their
+  // tail from ~80k to ~57k cycles but left the G warps three sub-partitions:
+  // G ~105k, 93.6 vs 90.5 ms per 1M C3 instances.)
+  const bool lteam = w >= CFB_PIPE_GW_;
+  const int lw = w - CFB_PIPE_GW_;  // rank among the front/tail warps
+  const int gw = w;                 // rank among the G warps
   if (!lteam) {  // G team
     const Team T{gw * 32 + (int)(threadIdx.x & 31), kPipeGT, gw, 1};
     for (int i = 0;; ++i) {
