@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(PipeShape<S>::T, PipeShape<S>::MINB) solve_pip
         }
         PIPE_T0
         const long long k = kb[b];
-        solve_one<N, false, false, PH_TAIL>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T, gbuf(b));
+        solve_one<N, false, false, PH_TAIL, PS::LW>(a, k, (size_t)k * M, M, input(k), sm + b * bufb, a.L, T,
+                                                    gbuf(b));
         PIPE_ACC(3)
       }
       if (stop == INT_MAX) produce();
