@@ -16,7 +16,8 @@ for M, K, lo, hi in [(50, 64, 0.25, 1.0), (20, 32, 0.5, 3.0), (100, 4, 0.25, 1.0
     print("small path ok", M, K, flush=True)
 # the pipelined persistent kernel (K >= 2048, M <= 64): teams, named barriers,
 # mbarriers, the L2 G tables
-for M, K, lo, hi, light in [(50, 2100, 0.25, 1.0, False), (20, 2048, 0.05, 0.2, True), (64, 2048, 0.25, 1.0, False)]:
+for M, K, lo, hi, light in [(50, 2100, 0.25, 1.0, False), (20, 2048, 0.05, 0.2, True), (64, 2048, 0.25, 1.0, False),
+                             (100, 2048, 0.25, 1.0, False)]:
     prof = profile_light(M) if light else profile_heavy(M)
     u = sample_batch(K, M, prof, lo, hi, seed=M + 7)
     ip, og = eng.sweep(prof, u)

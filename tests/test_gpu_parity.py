@@ -167,6 +167,15 @@ def test_pipelined_kernel_shapes(engine, M, K, light):
         ck.assert_same_og({k: v[k0:k1] for k, v in og.items()}, ck.oracle_og(prof, sub), where=f"M={M} [{k0},{k1})")
 
 
+def test_pipelined_kernel_single_solver(engine):
+    """IP-SSA alone and OG alone through the pipelined kernel (>= 2048
+    instances): the G phase runs only that solver's chains."""
+    prof = profile_heavy(50)
+    users = sample_batch(2048, 50, prof, 0.25, 1.0, seed=77)
+    ck.assert_same_ip(engine.ipssa(prof, users), ck.oracle_ipssa(prof, users), where="ipssa only")
+    ck.assert_same_og(engine.og(prof, users), ck.oracle_og(prof, users), where="og only")
+
+
 def test_light_profile_online_shape(engine):
     prof = profile_light(14)
     users = sample_batch(512, 14, prof, 0.05, 0.2, seed=12)
