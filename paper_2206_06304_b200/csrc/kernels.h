@@ -172,6 +172,13 @@ bool pipe_fits(int M, int N);
 // the instances each keeps in flight per SM; measured crossovers, see there)
 bool pipe_preferred(int M, int N);
 size_t pipe_gg_doubles(int M, int N);  // the global G-table workspace the pipelined kernel wants
+// per team shape (solve_pipe{0,1,2}.cu): resident CTAs, launch
+int pipe_max_grid_s0(int M, int N);
+int pipe_max_grid_s1(int M, int N);
+int pipe_max_grid_s2(int M, int N);
+cudaError_t launch_pipe_s0(const SmallArgs& a, cudaStream_t st);
+cudaError_t launch_pipe_s1(const SmallArgs& a, cudaStream_t st);
+cudaError_t launch_pipe_s2(const SmallArgs& a, cudaStream_t st);
 cudaError_t launch_fixed(const SmallArgs& a, const int32_t* b, int grid, cudaStream_t st);
 
 #ifdef CFB_ONLY_N  // development builds: one sub-task count only (fast compiles)

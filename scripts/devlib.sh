@@ -9,7 +9,7 @@ F="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false
 T=/tmp/devobj_$$
 mkdir -p $T ../../build
 pids=()
-for f in capi solve_small solve_large online probe baselines generate oracles; do
+for f in capi solve_small solve_pipe0 solve_pipe1 solve_pipe2 solve_large online probe baselines generate oracles; do
   nvcc $F -c $f.cu -o $T/$f.o & pids+=($!)
 done
 for p in "${pids[@]}"; do wait $p; done

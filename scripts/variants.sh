@@ -17,9 +17,12 @@ done
 wait
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
-  ( nvcc $F $flags -Xptxas -v -c $SRC/solve_small.cu -o $ROOT/build/_var_$name.o 2> $ROOT/build/var_$name.ptxas.log &&
+  ( nvcc $F $flags -Xptxas -v -c $SRC/solve_small.cu -o $ROOT/build/_var_$name.o 2> $ROOT/build/var_$name.ptxas.log &
+    for sh in 0 1 2; do nvcc $F $flags -c $SRC/solve_pipe$sh.cu -o $ROOT/build/_var_${name}_p$sh.o 2>> $ROOT/build/var_$name.pipe.log & done
+    wait
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/build/var_$name.so $ROOT/build/_var_$name.o \
+      $ROOT/build/_var_${name}_p{0,1,2}.o \
       $ROOT/build/_common/{capi,solve_large,online,probe,baselines,generate,oracles}.o -lcudart &&
-    echo "built var_$name: $(grep -A2 'solve_small_kernelILi4' $ROOT/build/var_$name.ptxas.log | grep -o '[0-9]* bytes spill stores' | head -1)" ) &
+    echo "built var_$name" ) &
 done
 wait
