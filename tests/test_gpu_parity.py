@@ -176,6 +176,23 @@ def test_pipelined_kernel_single_solver(engine):
     ck.assert_same_og(engine.og(prof, users), ck.oracle_og(prof, users), where="og only")
 
 
+def test_pipelined_kernel_invalid_and_infeasible_instances(engine):
+    """Instances that fail Scenario::check, or have no feasible plan, inside a
+    pipelined batch: their statuses, and every other instance's solution."""
+    prof = profile_heavy(50)
+    users = sample_batch(2048, 50, prof, 0.25, 1.0, seed=91)
+    users = {k: v.copy() for k, v in users.items()}
+    users["kappa"][3, 7] = -1.0          # COINFER_ST_NEG_KAPPA
+    users["rate_up"][100, 0] = 0.0       # bad rate
+    users["deadline"][777, 5] = users["arrival"][777, 5]  # deadline not after arrival
+    users["deadline"][1500, :] = 1e-9    # nobody can finish: infeasible
+    users["f_max"][2047, 3] = -2.0       # bad frequency
+    ip, og = engine.sweep(prof, users)
+    ck.assert_same_ip(ip, ck.oracle_ipssa(prof, users), where="pipelined, invalid rows")
+    ck.assert_same_og(og, ck.oracle_og(prof, users), where="pipelined, invalid rows")
+    assert (np.asarray(og["status"])[[3, 100, 777, 2047]] != 0).all()
+
+
 def test_light_profile_online_shape(engine):
     prof = profile_light(14)
     users = sample_batch(512, 14, prof, 0.05, 0.2, seed=12)
