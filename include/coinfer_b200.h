@@ -272,7 +272,9 @@ int coinfer_sweep_batch(coinfer_ctx* ctx, const coinfer_profile* profile,
    with work counters -- counters[0] OG chain steps ((user, chain)
    evaluations), [1] IP-SSA chain steps, [2] all-local user steps, [3] b*
    re-derivation steps, [4] chain starts (start-time recursions), [5] DP
-   cells, [6] instances, [7] reserved.  Decisions are the solver's; M <= 255
+   cells, [6] instances, [7] the b* steps of instances
+   whose groups do not all take their largest admissible bound (the
+   pipelined kernel's speculative b* re-runs only those).  Decisions are the solver's; M <= 255
    (the shared-memory path). */
 int coinfer_count_work(coinfer_ctx* ctx, const coinfer_profile* profile, const coinfer_users* users,
                        coinfer_ipssa_out* ipssa, coinfer_og_out* og, uint64_t* counters);

@@ -40,7 +40,7 @@ struct SmallArgs {
   // pipelined kernel: G tables in global memory, 2 per CTA (pipe_gg_doubles), or NULL
   double* gg;
 };
-enum { CTR_OG = 0, CTR_IP, CTR_LOCAL, CTR_BSTAR, CTR_STARTS, CTR_DP, CTR_INST, CTR_N = 8 };
+enum { CTR_OG = 0, CTR_IP, CTR_LOCAL, CTR_BSTAR, CTR_STARTS, CTR_DP, CTR_INST, CTR_BSTAR_MISS, CTR_N = 8 };
 
 // One instance's users (global or shared memory), already offset.
 struct InstIn {

@@ -418,7 +418,7 @@ class Engine:
         return Packed.arrays(pk.out_ip), Packed.arrays(pk.out_og)
 
     COUNTERS = ["og_chain_steps", "ip_chain_steps", "local_steps", "bstar_steps", "chain_starts",
-                "dp_cells", "instances"]
+                "dp_cells", "instances", "bstar_miss_steps"]
 
     def count_work(self, profile, users: Dict):
         """The fused sweep's executed work units (coinfer_count_work: the

@@ -7,6 +7,7 @@ from paper_2206_06304_b200 import Engine, profile_heavy, sub_seed
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 eng = Engine(0)
+eng.set_stream(torch.cuda.current_stream())  # events on the launching stream
 prof = profile_heavy(M)
 u, st = eng.sample(prof, M, sub_seed(1, 1, np.arange(K, dtype=np.uint64)), 0.25, 1.0, device=True)
 dev = {k: u[k] for k in ["f_min", "f_max", "kappa", "rate_up", "power_up", "arrival", "deadline"]}

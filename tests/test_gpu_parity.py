@@ -296,3 +296,12 @@ def test_count_work_counts_the_same_solve(engine):
     assert a["instances"] == 300
     assert a["og_chain_steps"] >= a["chain_starts"] > 0 and a["ip_chain_steps"] > 0
     assert a["dp_cells"] > 0 and a["bstar_steps"] > 0
+    # [7]: the b* steps of instances whose groups do not all take their
+    # largest admissible bound (group_b == group_size), the instances where
+    # the pipelined kernel's speculative b* falls back to the full pass
+    ip, og = engine.sweep(prof, users)
+    miss = [k for k in range(300) if og["status"][k] == 0 and not og["fallback"][k]
+            and any(og["group_b"][k][g] != og["group_size"][k][g] for g in range(og["n_groups"][k]))]
+    assert 0 <= a["bstar_miss_steps"] <= a["bstar_steps"]
+    assert (a["bstar_miss_steps"] > 0) == (len(miss) > 0)
+    assert 0 < len(miss) < 300  # both branches occur at this size
