@@ -23,6 +23,8 @@
 // G, the prefix minima (St) and the u16 triangles are upper triangles in
 // global memory, row-major.
 
+#include <type_traits>
+
 #include "solve_core.cuh"
 
 namespace cfb {
@@ -35,6 +37,10 @@ __device__ __forceinline__ long long tri_u(long long i, long long j, long long M
 [[maybe_unused]] __device__ __forceinline__ long long tri_l(long long j, long long p) {
   return ((j * (j + 1)) >> 1) + p;  // lower triangle: row j holds p = 0..j
 }
+
+// fast DP (large_dp): rows of <= kFastDW useful cells, live columns in a
+// shared-memory ring of kFastDR slots
+constexpr int kFastDW = 96, kFastDR = 128;
 
 }  // namespace
 
@@ -260,6 +266,243 @@ extern "C" int coinfer_debug_large_times(unsigned long long* out) {
   return 0;
 }
 #endif
+// The grouping DP when every row i >= 1 has <= kFastDW useful cells (C4:
+// ~35, peaks in the 70s), one warp, one row per stage (offline_solvers.hpp:
+// 313-330).  Column c's useful rows are row 0 and a suffix [q1(c), c], so
+// its prefix minima live dense over that suffix: S0[c] (row 0) below
+// q1(c), then one entry per row; only columns i-1 .. i+DW are live at
+// stage i, so they sit in a ring of DR column slots.
+//   Stage i needs column i-1 complete and nothing else new: its critical
+// path is one shared load of column i-1 and of each cell's running
+// minimum, an add, a compare and the stores.  One warp runs it, so every
+// dependency is exposed: the stage is straight-line code over only the
+// row's live 32-cell chunks (stores of lanes past the row go to a dummy
+// slot instead of branching), the parent's tie check (rounding that merges
+// an earlier, larger S into the same sum) reads column i-1 beside the
+// critical chain, and the row's G / pfit come from a shared-memory ring
+// that cp.async fills kPD rows ahead (the completion counter, not a
+// register scoreboard, tracks them), read into registers one stage ahead.
+namespace {
+constexpr int kPD = 8;  // rows of G / pfit in flight (power of 2)
+struct DpIn {  // one stage's inputs, per lane: cells i + 32c + lane
+  double g[3], s0j[3];
+  int p[3], qj[3];
+  int rl, q1c;
+  double s0c;
+};
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" : : "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" : : "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" : : : "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" : : "n"(K) : "memory"); }
+// large_dp's shared memory: S0 | ring values (+1 dummy) | running values
+// (+1 dummy) | ring positions | running positions | q1 | rlen | staged G |
+// staged pfit words
+struct DpSmem {
+  int oRingV, oRunV, oRingA, oRunA, oQ1, oRl, oStG, oStP, bytes;
+  __host__ __device__ explicit DpSmem(int M) {
+    auto al = [](int x) { return (x + 15) & ~15; };
+    oRingV = al(8 * M);
+    oRunV = al(oRingV + 8 * (kFastDR * kFastDW + 1));
+    oRingA = al(oRunV + 8 * (kFastDR + 1));
+    oRunA = al(oRingA + 2 * (kFastDR * kFastDW + 1));
+    oQ1 = al(oRunA + 2 * (kFastDR + 1));
+    oRl = al(oQ1 + 2 * M);
+    oStG = al(oRl + 2 * M);
+    oStP = al(oStG + 8 * kPD * kFastDW);
+    bytes = al(oStP + 4 * kPD * kFastDW);
+  }
+};
+}  // namespace
+
+__global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
+  if (*a.status != INT_MAX) return;
+  extern __shared__ __align__(16) unsigned char smb[];
+  constexpr int DW = kFastDW, DR = kFastDR;
+  const int M = a.M, tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+  __shared__ int ired[8];
+  int rlmax = 0;
+  for (int j = 1 + tid; j < M; j += NT) rlmax = max(rlmax, a.rlen[j]);
+  rlmax = __reduce_max_sync(kFull, rlmax);
+  if (lane == 0) ired[warp] = rlmax;
+  __syncthreads();
+  rlmax = 0;
+  for (int w = 0; w < NW; ++w) rlmax = max(rlmax, ired[w]);
+  if (rlmax > DW) return;  // large_finish runs the change-point DP
+  const double INF = dinf();
+  const DpSmem L(M);
+  double* S0 = reinterpret_cast<double*>(smb);                   // [M] row 0: S = G = PM
+  double* ringV = reinterpret_cast<double*>(smb + L.oRingV);      // [DR*DW] PM_c over rows q1(c).. | dummy
+  double* runV = reinterpret_cast<double*>(smb + L.oRunV);        // [DR] running PM of live columns | dummy
+  uint16_t* ringA = reinterpret_cast<uint16_t*>(smb + L.oRingA);  // first positions of the PMs
+  uint16_t* runA = reinterpret_cast<uint16_t*>(smb + L.oRunA);
+  uint16_t* q1 = reinterpret_cast<uint16_t*>(smb + L.oQ1);        // [M] first useful row >= 1 per column (M: none)
+  uint16_t* rlS = reinterpret_cast<uint16_t*>(smb + L.oRl);       // [M] useful row lengths
+  double* stG = reinterpret_cast<double*>(smb + L.oStG);          // [kPD*DW] staged G rows
+  uint32_t* stP = reinterpret_cast<uint32_t*>(smb + L.oStP);      // [kPD*DW] staged pfit words
+  for (int j = tid; j < M; j += NT) {
+    S0[j] = a.G[tri_u(0, j, M)];
+    a.par[tri_u(0, j, M)] = 0xffff;
+    q1[j] = (uint16_t)M;
+    rlS[j] = (uint16_t)a.rlen[j];
+  }
+  if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
+  __syncthreads();
+  for (int q = 1 + tid; q < M; q += NT) {  // columns whose first useful row >= 1 is q
+    const int e0 = q == 1 ? 1 : (q - 1) + a.rlen[q - 1], e1 = q + a.rlen[q];
+    for (int c = max(e0, 1); c < e1 && c < M; ++c) q1[c] = (uint16_t)q;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  const double* __restrict__ G = a.G;
+  const uint16_t* __restrict__ PF = a.pfit;
+  uint16_t* __restrict__ PAR = a.par;
+  // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j
+  auto xrow = [&](int i) {
+    const uint32_t ui = (uint32_t)i;
+    return ui * (uint32_t)M - ui * (ui - 1u) / 2u - ui;
+  };
+  auto issue = [&](int r) {  // cp.async row r's cells (all three chunks; the row runs to M-1)
+    if (r < M) {
+      const int s = (r & (kPD - 1)) * DW;
+      const uint32_t xr = xrow(r);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t x = xr + (uint32_t)min(r + 32 * c + lane, M - 1);
+        cp_async8(stG + s + 32 * c + lane, G + x);
+        cp_async4(stP + s + 32 * c + lane,
+                  reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(PF + x) & ~(uintptr_t)3));
+      }
+    }
+    cp_async_commit();
+  };
+  auto fetch = [&](DpIn& R, int i) {  // row i's inputs into registers (its cp.async group has landed)
+    if (i >= M) return;
+    const int s = (i & (kPD - 1)) * DW;
+    const uint32_t xr = xrow(i);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int j = min(i + 32 * c + lane, M - 1);
+      R.g[c] = stG[s + 32 * c + lane];
+      R.p[c] = (int)((stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu);
+      R.qj[c] = q1[j];
+      R.s0j[c] = S0[j];
+    }
+    R.rl = rlS[i];
+    R.q1c = q1[i - 1];
+    R.s0c = S0[i - 1];
+  };
+  auto stage = [&](const DpIn& R, int i, auto nc_tag) {
+    constexpr int NC = decltype(nc_tag)::value;
+    const int jend = i + R.rl, q1c = R.q1c;
+    const double s0c = R.s0c;
+    const int cs = ((i - 1) & (DR - 1)) * DW - q1c;  // column i-1: entry of row r at cs + r, r >= q1c
+    double best[NC], cand[NC], vC[NC], vR[NC], npm[NC];
+    int bp[NC], aC[NC], aR[NC], na[NC], ws[NC], wr[NC];
+    bool tie[NC];
+    // all loads of the stage first (the compiler cannot move a load of one
+    // chunk above a store of another), then the selects, then the stores
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int slot = min(i + 32 * c + lane, M - 1) & (DR - 1), rc = max(R.p[c] - 1, q1c);
+      vC[c] = ringV[cs + rc];
+      aC[c] = ringA[cs + rc];
+      vR[c] = runV[slot];
+      aR[c] = runA[slot];
+    }
+    double vT[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int pma = R.p[c] - 1 < q1c ? 0 : aC[c];
+      vT[c] = ringV[cs + max(pma - 1, q1c)];  // the row before the minimum's first position
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int jt = i + 32 * c + lane, slot = min(jt, M - 1) & (DR - 1);
+      const bool in = jt < jend;
+      const int p = R.p[c], r = p - 1;
+      const double rv = r < q1c ? s0c : vC[c];
+      const int pma = r < q1c ? 0 : aC[c];
+      const bool first = i == R.qj[c];
+      const double pmj = first ? R.s0j[c] : vR[c];
+      const int paj = first ? 0 : aR[c];
+      const double g = R.g[c];
+      const bool valid = in && g != INF && p > 0;
+      cand[c] = __dadd_rn(rv, g);
+      best[c] = valid ? cand[c] : INF;   // (rv = INF gives cand = INF)
+      const bool lower = best[c] < pmj;  // strict: the first position is kept
+      npm[c] = lower ? best[c] : pmj;
+      na[c] = lower ? i : paj;
+      ws[c] = in ? slot : DR;  // lanes past the row store to the dummy slot
+      wr[c] = in ? slot * DW + (i - R.qj[c]) : DR * DW;
+      const bool fin = valid && cand[c] != INF;
+      bp[c] = fin ? pma : 0xffff;
+      tie[c] = fin && pma > 0 && __dadd_rn(pma - 1 < q1c ? s0c : vT[c], g) == cand[c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      runV[ws[c]] = npm[c];
+      runA[ws[c]] = (uint16_t)na[c];
+      ringV[wr[c]] = npm[c];
+      ringA[wr[c]] = (uint16_t)na[c];
+    }
+    bool anytie = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) anytie = anytie || tie[c];
+    if (__any_sync(kFull, anytie)) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (tie[c]) {  // the first row whose S sums to the same value
+          const double g = R.g[c];
+          int qa = 0, qb = bp[c] - 1;
+          while (qa < qb) {
+            const int mid = (qa + qb) >> 1;
+            if (__dadd_rn(mid < q1c ? s0c : ringV[cs + mid], g) == cand[c]) qb = mid; else qa = mid + 1;
+          }
+          bp[c] = qb;
+        }
+    }
+    const uint32_t xr = xrow(i);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int jt = i + 32 * c + lane;
+      if (jt < jend) {
+        PAR[xr + (uint32_t)jt] = (uint16_t)bp[c];
+        if (jt == M - 1) a.slast[i] = best[c];
+      }
+    }
+  };
+  auto step = [&](const DpIn& cur, DpIn& nxt, int i) {
+    if (lane == 0 && i + cur.rl < M) a.slast[i] = INF;
+    switch ((cur.rl + 31) >> 5) {
+      case 1: stage(cur, i, std::integral_constant<int, 1>{}); break;
+      case 2: stage(cur, i, std::integral_constant<int, 2>{}); break;
+      case 3: stage(cur, i, std::integral_constant<int, 3>{}); break;
+      default: break;  // no useful cell
+    }
+    issue(i + kPD);                // into row i's slot (read by fetch(cur, i))
+    cp_async_wait<kPD - 1>();      // row i + 1 has landed
+    fetch(nxt, i + 1);
+    __syncwarp();
+  };
+  for (int r = 1; r <= kPD; ++r) issue(r);
+  cp_async_wait<kPD - 1>();
+  DpIn A, B;
+  fetch(A, 1);
+  for (int i = 1; i < M; i += 2) {
+    step(A, B, i);
+    if (i + 1 >= M) break;
+    step(B, A, i + 1);
+  }
+  cp_async_wait<0>();
+}
+
 template <int N>
 __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   using R = Rec<N>;
@@ -365,9 +608,8 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   // per row -- the small path's in-place scheme (solve_core.cuh) with O(1)
   // lookups instead of change-point searches.  Only columns i-1 .. i+DW are
   // live at stage i, so they sit in a shared-memory ring of DR columns.
-  // Warp 0 runs the stages, one __syncwarp each, the next row's G / pfit
-  // loads in flight.
-  constexpr int DW = 96, DR = 128;
+  // That DP is its own kernel, large_dp (below), launched just before this
+  // one; it and this kernel take the same decision from the row lengths.
   int rlmax = 0;
   for (int j = 1 + tid; j < M; j += NT) rlmax = max(rlmax, a.rlen[j]);
   rlmax = __reduce_max_sync(kFull, rlmax);
@@ -376,119 +618,9 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   rlmax = 0;
   for (int w = 0; w < NW; ++w) rlmax = max(rlmax, ired[w]);
   __syncthreads();
-  const bool fastdp = rlmax <= DW;
+  const bool fastdp = rlmax <= kFastDW;
   if (fastdp) {
-    double* S0 = reinterpret_cast<double*>(smb);        // [M] row 0: S = G = PM
-    double* ringV = S0 + M;                             // [DR*DW] PM_c over rows q1(c)..
-    double* runV = ringV + DR * DW;                     // [DR] running PM of live columns
-    uint16_t* ringA = reinterpret_cast<uint16_t*>(runV + DR);  // [DR*DW] first position of PM
-    uint16_t* runA = ringA + DR * DW;                   // [DR]
-    uint16_t* q1 = runA + DR;                           // [M] first useful row >= 1 per column (M: none)
-    uint16_t* rlS = q1 + M;                             // [M] useful row lengths
-    for (int j = tid; j < M; j += NT) {
-      const double g = a.G[tri_u(0, j, M)];
-      S0[j] = g;
-      a.par[tri_u(0, j, M)] = 0xffff;
-      q1[j] = (uint16_t)M;
-      rlS[j] = (uint16_t)a.rlen[j];
-    }
-    if (tid == 0) a.slast[0] = a.G[tri_u(0, M - 1, M)];
-    __syncthreads();
-    for (int q = 1 + tid; q < M; q += NT) {  // columns whose first useful row >= 1 is q
-      const int e0 = q == 1 ? 1 : (q - 1) + a.rlen[q - 1], e1 = q + a.rlen[q];
-      for (int c = max(e0, 1); c < e1 && c < M; ++c) q1[c] = (uint16_t)q;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j,
-      // xr(i) = i*M - i(i-1)/2 - i, advanced by M - 1 - i per row
-      const double* __restrict__ G = a.G;
-      const uint16_t* __restrict__ PF = a.pfit;
-      uint16_t* __restrict__ PAR = a.par;
-      double gq[3], gc[3];
-      int pq[3], pc[3];
-      uint32_t xr = (uint32_t)M - 1u;  // row 1
-      auto prefetch = [&](int r, uint32_t xrr) {
-        const int je = r + rlS[r];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int j = r + 32 * c + lane;
-          gq[c] = j < je ? G[xrr + (uint32_t)j] : INF;
-          pq[c] = j < je ? PF[xrr + (uint32_t)j] : 0;
-        }
-      };
-      prefetch(1, xr);
-      for (int i = 1; i < M; ++i, xr += (uint32_t)(M - i)) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          gc[c] = gq[c];
-          pc[c] = pq[c];
-        }
-        if (i + 1 < M) prefetch(i + 1, xr + (uint32_t)(M - 1 - i));  // in flight during this stage
-        const int rl = rlS[i], jend = i + rl;
-        if (lane == 0 && jend < M) a.slast[i] = INF;
-        const int cr = i - 1, q1c = q1[cr];
-        const double s0c = S0[cr];
-        const double* colV = ringV + (cr & (DR - 1)) * DW - q1c;  // colV[r], r >= q1c
-        const uint16_t* colA = ringA + (cr & (DR - 1)) * DW - q1c;
-        // all loads of the stage first (independent), then the decisions, then the stores
-        double rv[3], pmj[3];
-        int pma[3], qjv[3], paj[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int j = min(i + 32 * c + lane, M - 1);
-          const int r = max(pc[c] - 1, 0);
-          rv[c] = r < q1c ? s0c : colV[r];
-          pma[c] = r < q1c ? 0 : colA[r];
-          const int slot = j & (DR - 1), qj = q1[j];
-          qjv[c] = qj;
-          // (clamped lanes past the row read nothing: another lane owns slot M-1)
-          const bool own = i + 32 * c + lane < M;
-          pmj[c] = !own ? INF : i == qj ? S0[j] : runV[slot];
-          paj[c] = !own ? 0 : i == qj ? 0 : runA[slot];
-        }
-        double best[3];
-        int bp[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double g = gc[c];
-          best[c] = INF;
-          bp[c] = 0xffff;
-          if (g != INF && pc[c] > 0) {
-            const double cand = __dadd_rn(rv[c], g);
-            if (cand != INF) {
-              best[c] = cand;
-              int qb = pma[c];
-              if (qb > 0 && __dadd_rn(qb - 1 < q1c ? s0c : colV[qb - 1], g) == cand) {
-                int qa = 0;  // rounding merged an earlier, larger S: first such row
-                --qb;
-                while (qa < qb) {
-                  const int mid = (qa + qb) >> 1;
-                  if (__dadd_rn(mid < q1c ? s0c : colV[mid], g) == cand) qb = mid; else qa = mid + 1;
-                }
-              }
-              bp[c] = qb;
-            }
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int j = i + 32 * c + lane;
-          if (j >= jend) continue;
-          if (j == M - 1) a.slast[i] = best[c];
-          PAR[xr + (uint32_t)j] = (uint16_t)bp[c];
-          const int slot = j & (DR - 1), qj = qjv[c];
-          const bool lower = best[c] < pmj[c];  // strict: the first position is kept
-          const double npm = lower ? best[c] : pmj[c];
-          const int na = lower ? i : paj[c];
-          runV[slot] = npm;
-          runA[slot] = (uint16_t)na;
-          ringV[slot * DW + (i - qj)] = npm;
-          ringA[slot * DW + (i - qj)] = (uint16_t)na;
-        }
-        __syncwarp();
-      }
-    }
+    // the whole DP ran in large_dp (same rlmax test): S row M-1 in slast, parents in par
   } else {
     double* chgV = a.St;
     uint16_t* chgR = a.argpm;
@@ -795,8 +927,14 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   }
   __syncthreads();
   const int ng = s_ng;
-  for (int g = tid; g < ng; g += NT)
-    for (int x = gl[g]; x <= gh[g]; ++x) a.gid[x] = g;
+  for (int x = tid; x < M; x += NT) {  // the group holding sorted user x: the last lo <= x
+    int g0 = 0, g1 = ng - 1;
+    while (g0 < g1) {
+      const int mid = (g0 + g1 + 1) >> 1;
+      if (gl[mid] <= x) g0 = mid; else g1 = mid - 1;
+    }
+    a.gid[x] = g0;
+  }
   __syncthreads();
   // stitch: re-derive each chosen group's plan from its stored bound
   for (int x = tid; x < M; x += NT) {
@@ -822,23 +960,58 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
     if (a.og.user_energy) a.og.user_energy[base + m] = fold<N>(r, sp, f, 0.0);
   }
   __syncthreads();
-  for (int g = tid; g < ng; g += NT) {
+  // group energies and batch sizes: one warp per group, 32 members at a
+  // time; each lane computes its member's terms (fold<N>'s products), and
+  // every lane runs the group's left fold over them in member order through
+  // shuffles (the adds are the only serial part)
+  for (int g = warp; g < ng; g += NW) {
     const int lo = gl[g], hi = gh[g];
     double total = 0.0;
-    for (int x = lo; x <= hi; ++x) total = fold<N>(a.rec + (size_t)x * R::SIZE, a.spos[x], a.fpos[x], total);
-    a.genergy[g] = total;
-    const size_t gi = base + g;
-    if (a.og.group_lo) a.og.group_lo[gi] = lo;
-    if (a.og.group_size) a.og.group_size[gi] = hi - lo + 1;
-    if (a.og.group_b) a.og.group_b[gi] = a.bstar[tri_u(lo, hi, M)];
-    if (a.og.group_deadline) a.og.group_deadline[gi] = dls[lo];
-    if (a.og.group_energy) a.og.group_energy[gi] = total;
-    if (a.og.group_batch_size)
-      for (int n = 1; n <= N; ++n) {
-        int c = 0;
-        for (int x = lo; x <= hi; ++x) c += a.spos[x] < n;
-        a.og.group_batch_size[gi * N + n - 1] = c;
+    int cnt[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) cnt[n] = 0;
+    for (int x0 = lo; x0 <= hi; x0 += 32) {
+      const int x = x0 + lane;
+      const bool live = x <= hi;
+      double t[N + 1];
+      int sp = N;
+      if (live) {
+        const double* r = a.rec + (size_t)x * R::SIZE;
+        sp = a.spos[x];
+        const double f = a.fpos[x];
+#pragma unroll
+        for (int n = 1; n <= N; ++n) t[n - 1] = __dmul_rn(__dmul_rn(r[R::KA(n)], f), f);
+        t[N] = sp < N ? (sp == 0 ? r[R::E0] : r[R::U(sp)]) : 0.0;
+      } else {
+#pragma unroll
+        for (int n = 0; n <= N; ++n) t[n] = 0.0;
       }
+      const int nu = min(32, hi - x0 + 1);
+      for (int u = 0; u < nu; ++u) {
+        const int su = __shfl_sync(kFull, sp, u);
+#pragma unroll
+        for (int n = 1; n <= N; ++n) {
+          const double tv = __shfl_sync(kFull, t[n - 1], u);
+          if (n <= su) total = __dadd_rn(total, tv);
+        }
+        const double up = __shfl_sync(kFull, t[N], u);
+        if (su < N) total = __dadd_rn(total, up);
+      }
+#pragma unroll
+      for (int n = 1; n <= N; ++n) cnt[n - 1] += __popc(__ballot_sync(kFull, live && sp < n));
+    }
+    if (lane == 0) {
+      a.genergy[g] = total;
+      const size_t gi = base + g;
+      if (a.og.group_lo) a.og.group_lo[gi] = lo;
+      if (a.og.group_size) a.og.group_size[gi] = hi - lo + 1;
+      if (a.og.group_b) a.og.group_b[gi] = a.bstar[tri_u(lo, hi, M)];
+      if (a.og.group_deadline) a.og.group_deadline[gi] = dls[lo];
+      if (a.og.group_energy) a.og.group_energy[gi] = total;
+      if (a.og.group_batch_size)
+#pragma unroll
+        for (int n = 1; n <= N; ++n) a.og.group_batch_size[gi * N + n - 1] = cnt[n - 1];
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -903,13 +1076,17 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
     const int g = (int)((T + 255) / 256 < 148 * 8 ? (T + 255) / 256 : 148 * 8);
     large_pfit<<<g, 256, 0, st>>>(a);
   }
-  // running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
-  // fast DP ring: S0 | ring values | running values | ring positions | running positions | q1 | rlen
-  const int smem_fast = 8 * M + 128 * 96 * 8 + 128 * 8 + 128 * 96 * 2 + 128 * 2 + 2 * 2 * M;
-  const int smem_old = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
-  const int smem = smem_fast > smem_old ? smem_fast : smem_old;
-  if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
-  cudaError_t e = ensure_smem((const void*)large_finish<N>, smem);
+  const int smem_fast = DpSmem(M).bytes;  // large_dp
+  // large_finish: running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
+  const int smem = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
+  if (M > 8 * 1024 || smem > 227 * 1024 || smem_fast > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
+  cudaError_t e;
+  if (a.do_og) {
+    e = ensure_smem((const void*)large_dp, smem_fast);
+    if (e != cudaSuccess) return e;
+    large_dp<<<1, 256, smem_fast, st>>>(a);
+  }
+  e = ensure_smem((const void*)large_finish<N>, smem);
   if (e != cudaSuccess) return e;
   large_finish<N><<<1, 1024, smem, st>>>(a);
   return cudaGetLastError();

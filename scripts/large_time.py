@@ -11,5 +11,9 @@ eng.og(prof, dev); torch.cuda.synchronize()
 buf = (C.c_ulonglong * 8)()
 _abi.load_library().coinfer_debug_large_times(buf)
 n = buf[3]
-print(f"short stages {n}, staged from global {buf[4]}; cycles per stage: setup+column {buf[0]/n:.0f}, "
-      f"wait for G/pfit {buf[1]/n:.0f}, cells+sync {buf[2]/n:.0f}")
+if n:
+  print(f"short stages {n}, staged from global {buf[4]}; cycles per stage: setup+column {buf[0]/n:.0f}, "
+        f"wait for G/pfit {buf[1]/n:.0f}, cells+sync {buf[2]/n:.0f}")
+if buf[7]:
+    print(f"fast DP stages {buf[7]}: cycles per stage issue+wait+read G/pfit {buf[5]/buf[7]:.0f}, "
+          f"cells+stores+sync {buf[6]/buf[7]:.0f}")
