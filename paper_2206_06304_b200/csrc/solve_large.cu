@@ -4,7 +4,7 @@
 // Same algorithm and bit-exact semantics as solve_core.cuh (see the comments
 // there and in solve_small.cu); only the data placement and the work split
 // differ:
-//   large_prep    one thread per user: contract check, stable deadline rank,
+//   large_prep    one warp per user: contract check, stable deadline rank,
 //                 hoisted records (global, sorted order), sum_latency table
 //   large_rows    one thread per row: first infeasible bound b0 (row 0 is the
 //                 IP-SSA row when requested)
@@ -12,9 +12,11 @@
 //                 passes of 32 lanes, each pass one left fold over j; the
 //                 warp-wide lexicographic argmin (energy asc, b desc) per cell
 //                 merges into the row with `<=` (later passes carry larger b)
-//   large_pfit    one thread per DP cell: the feasible-prev prefix length
-//                 (groups_fit is monotone in prev), before the DP
-//   large_finish  one CTA: the grouping DP over M sequential stages
+//   large_pfit    one warp per row, a lane per useful DP cell: the
+//                 feasible-prev prefix length (groups_fit is monotone in prev)
+//   large_dp      one warp: the grouping DP over M sequential stages when
+//                 every row has <= 96 useful cells (dense prefix-minimum ring)
+//   large_finish  one CTA: otherwise the grouping DP over M sequential stages
 //                 (offline_solvers.hpp:313-330), the same O(1)-per-cell scheme
 //                 as solve_core.cuh: the triangle holds column prefix minima
 //                 and their first positions (running values of each column in
@@ -50,30 +52,33 @@ __device__ __forceinline__ double ip_deadline(const LargeArgs& a, double dflt) {
 }
 
 template <int N>
-__global__ void large_prep(LargeArgs a) {
+__global__ void large_prep(LargeArgs a) {  // one warp per user m (and per sumlat entry m)
   using R = Rec<N>;
   const int M = a.M;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (m < M) {
-    const double rd = a.rd ? a.rd[m] : 1.0, pd = a.pd ? a.pd[m] : 0.0;
-    const int code = check_user(a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], rd, a.pu[m], pd,
-                                a.arr[m], a.dl[m]);
-    if (code != COINFER_ST_OK && *a.status != COINFER_ST_SHORT_TABLE) atomicMin(a.status, m * 32 + code);
-    // SIMPLE path conditions (solve_core.cuh, device_common.cuh: fast_div_*)
-    if (!(a.arr[m] == 0.0 && a.fmin[m] == 0.0 && fast_div_deadline(a.dl[m]))) atomicAnd(a.simple, 0);
     const double d = a.dl[m];
     int r = 0;
-    for (int o = 0; o < M; ++o) {  // stable rank by (deadline, id), offline_solvers.hpp:292-296
+    for (int o = lane; o < M; o += 32) {  // stable rank by (deadline, id), offline_solvers.hpp:292-296
       const double e = __ldg(a.dl + o);
       r += (e < d) || (e == d && o < m);
     }
-    a.rank[m] = r;
-    a.order[r] = m;
-    a.dls[r] = d;
-    build_rec<N>(a.rec + (size_t)r * R::SIZE, a.P, a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], a.pu[m],
-                 a.arr[m], d);
+    r = __reduce_add_sync(kFull, r);
+    if (lane == 0) {
+      const double rd = a.rd ? a.rd[m] : 1.0, pd = a.pd ? a.pd[m] : 0.0;
+      const int code = check_user(a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], rd, a.pu[m], pd,
+                                  a.arr[m], a.dl[m]);
+      if (code != COINFER_ST_OK && *a.status != COINFER_ST_SHORT_TABLE) atomicMin(a.status, m * 32 + code);
+      // SIMPLE path conditions (solve_core.cuh, device_common.cuh: fast_div_*)
+      if (!(a.arr[m] == 0.0 && a.fmin[m] == 0.0 && fast_div_deadline(a.dl[m]))) atomicAnd(a.simple, 0);
+      a.rank[m] = r;
+      a.order[r] = m;
+      a.dls[r] = d;
+      build_rec<N>(a.rec + (size_t)r * R::SIZE, a.P, a.fmin[m], a.fmax[m], a.kappa[m], a.ru[m], a.pu[m],
+                   a.arr[m], d);
+    }
   }
-  if (m >= 1 && m <= M) {  // sum_latency(size = m), offline_solvers.hpp:42-47
+  if (lane == 0 && m >= 1 && m <= M) {  // sum_latency(size = m), offline_solvers.hpp:42-47
     double t = 0.0;
     for (int n = 1; n <= N; ++n) t = __dadd_rn(t, __ldg(a.lat + (size_t)(n - 1) * a.P.bmax + m - 1));
     a.sumlat[m] = t;
@@ -390,7 +395,8 @@ __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
     for (int c = 0; c < 3; ++c) {
       const int j = min(i + 32 * c + lane, M - 1);
       R.g[c] = stG[s + 32 * c + lane];
-      R.p[c] = (int)((stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu);
+      R.p[c] = i + 32 * c + lane < i + rlS[i]  // past the row's useful cells pfit is not computed
+                   ? (int)((stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu) : 0;
       R.qj[c] = q1[j];
       R.s0j[c] = S0[j];
     }
@@ -1034,26 +1040,22 @@ size_t large_ws_bytes(int M, int N) {
 
 // Feasible-prev prefix length of every DP cell (i >= 1): the number of prevs
 // in [0, i) with groups_fit(dl[prev], dl[i], j-i+1) (offline_solvers.hpp:229-232).
-__global__ void large_pfit(LargeArgs a) {
-  const int M = a.M;
-  const long long T = (long long)M * (M + 1) / 2;
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < T;
-       x += (long long)gridDim.x * blockDim.x) {
-    // row i of upper-triangle index x: largest i with tri_u(i, i) <= x
-    int lo = 0, hi = M - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tri_u(mid, mid, M) <= x) lo = mid; else hi = mid - 1;
+__global__ void large_pfit(LargeArgs a) {  // one warp per row i >= 1, its useful cells only
+  const int M = a.M, lane = threadIdx.x & 31;
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int i = 1 + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < M; i += nw) {
+    const int jend = i + a.rlen[i];  // past it no prev fits (pfit 0); no DP reads those cells
+    const double di = a.dls[i];
+    const long long xr = tri_u(i, i, M) - i;
+    for (int j = i + lane; j < jend; j += 32) {
+      const double thr = a.sumlat[j - i + 1];
+      int l2 = 0, h2 = i;  // useful: dls[0] + thr <= di, so prev 0 fits
+      while (l2 < h2) {
+        const int mid = (l2 + h2) >> 1;
+        if (__dadd_rn(a.dls[mid], thr) <= di) l2 = mid + 1; else h2 = mid;
+      }
+      a.pfit[xr + j] = (uint16_t)l2;
     }
-    const int i = lo, j = i + (int)(x - tri_u(i, i, M));
-    if (i == 0) continue;
-    const double thr = a.sumlat[j - i + 1], di = a.dls[i];
-    int l2 = 0, h2 = __dadd_rn(a.dls[0], thr) <= di ? i : 0;  // no prev fits: 0
-    while (l2 < h2) {
-      const int mid = (l2 + h2) >> 1;
-      if (__dadd_rn(a.dls[mid], thr) <= di) l2 = mid + 1; else h2 = mid;
-    }
-    a.pfit[x] = (uint16_t)l2;
   }
 }
 
@@ -1068,14 +1070,10 @@ template <int N>
 static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   const int M = a.M, Q = (a.do_ip ? 1 : 0) + (a.do_og ? M : 0);
   large_init<<<1, 1, 0, st>>>(a);
-  large_prep<N><<<(M + 256) / 256, 256, 0, st>>>(a);
+  large_prep<N><<<(M + 8) / 8, 256, 0, st>>>(a);  // warps for m = 0..M
   large_rows<N><<<(Q + 255) / 256, 256, 0, st>>>(a);
   large_grow<N><<<(Q + 3) / 4, 128, 0, st>>>(a);
-  if (a.do_og) {
-    const long long T = (long long)M * (M + 1) / 2;
-    const int g = (int)((T + 255) / 256 < 148 * 8 ? (T + 255) / 256 : 148 * 8);
-    large_pfit<<<g, 256, 0, st>>>(a);
-  }
+  if (a.do_og) large_pfit<<<(M + 7) / 8 < 148 * 8 ? (M + 7) / 8 : 148 * 8, 256, 0, st>>>(a);
   const int smem_fast = DpSmem(M).bytes;  // large_dp
   // large_finish: running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
   const int smem = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
