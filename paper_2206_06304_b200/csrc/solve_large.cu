@@ -289,12 +289,19 @@ extern "C" int coinfer_debug_large_times(unsigned long long* out) {
 // register scoreboard, tracks them), read into registers one stage ahead.
 namespace {
 constexpr int kPD = 8;  // rows of G / pfit in flight (power of 2)
-struct DpIn {  // one stage's inputs, per lane: cells i + 32c + lane
-  double g[3], s0j[3];
-  int p[3], qj[3];
+template <int NW>
+struct DpIn {  // one stage's inputs, per lane: cells i + 32(C0 + k) + lane of this warp's chunks
+  double g[NW], s0j[NW];
+  int p[NW], qj[NW];
   int rl, q1c;
   double s0c;
 };
+struct DpPtrs {  // large_dp's shared-memory arrays
+  double *S0, *ringV, *runV, *stG;
+  uint16_t *ringA, *runA, *q1, *rlS;
+  uint32_t* stP;
+};
+__device__ __forceinline__ void dp_bar() { asm volatile("bar.sync 1, 64;" : : : "memory"); }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" : : "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -326,10 +333,163 @@ struct DpSmem {
 };
 }  // namespace
 
+// One of large_dp's two warps: chunks C0 .. C0+NCW-1 (32 cells each) of
+// every row; the warps meet at a named barrier after each stage (a stage
+// reads ring entries the other warp wrote in the stages before).
+template <int C0, int NCW>
+__device__ __forceinline__ void dp_warp(const LargeArgs& a, const DpPtrs& sp, int lane) {
+  constexpr int DW = kFastDW, DR = kFastDR;
+  const int M = a.M;
+  const double INF = dinf();
+  double* __restrict__ ringV = sp.ringV;
+  double* __restrict__ runV = sp.runV;
+  uint16_t* __restrict__ ringA = sp.ringA;
+  uint16_t* __restrict__ runA = sp.runA;
+  const double* __restrict__ G = a.G;
+  const uint16_t* __restrict__ PF = a.pfit;
+  uint16_t* __restrict__ PAR = a.par;
+  // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j
+  auto xrow = [&](int i) {
+    const uint32_t ui = (uint32_t)i;
+    return ui * (uint32_t)M - ui * (ui - 1u) / 2u - ui;
+  };
+  auto issue = [&](int r) {  // cp.async this warp's cells of row r (the row runs to M-1)
+    if (r < M) {
+      const int s = (r & (kPD - 1)) * DW;
+      const uint32_t xr = xrow(r);
+#pragma unroll
+      for (int k = 0; k < NCW; ++k) {
+        const int c = C0 + k;
+        const uint32_t x = xr + (uint32_t)min(r + 32 * c + lane, M - 1);
+        cp_async8(sp.stG + s + 32 * c + lane, G + x);
+        cp_async4(sp.stP + s + 32 * c + lane,
+                  reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(PF + x) & ~(uintptr_t)3));
+      }
+    }
+    cp_async_commit();
+  };
+  auto fetch = [&](DpIn<NCW>& R, int i) {  // row i's inputs into registers (its cp.async group has landed)
+    if (i >= M) return;
+    const int s = (i & (kPD - 1)) * DW;
+    const uint32_t xr = xrow(i);
+    R.rl = sp.rlS[i];
+#pragma unroll
+    for (int k = 0; k < NCW; ++k) {
+      const int c = C0 + k, jt = i + 32 * c + lane, j = min(jt, M - 1);
+      R.g[k] = sp.stG[s + 32 * c + lane];
+      R.p[k] = jt < i + R.rl  // past the row's useful cells pfit is not computed
+                   ? (int)((sp.stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu) : 0;
+      R.qj[k] = sp.q1[j];
+      R.s0j[k] = sp.S0[j];
+    }
+    R.q1c = sp.q1[i - 1];
+    R.s0c = sp.S0[i - 1];
+  };
+  auto stage = [&](const DpIn<NCW>& R, int i, auto nc_tag) {
+    constexpr int NC = decltype(nc_tag)::value;  // live chunks of this warp
+    const int jend = i + R.rl, q1c = R.q1c;
+    const double s0c = R.s0c;
+    const int cs = ((i - 1) & (DR - 1)) * DW - q1c;  // column i-1: entry of row r at cs + r, r >= q1c
+    double best[NC], cand[NC], vC[NC], vR[NC], npm[NC], vT[NC];
+    int bp[NC], aC[NC], aR[NC], na[NC], ws[NC], wr[NC];
+    bool tie[NC];
+    // all loads of the stage first (the compiler cannot move a load of one
+    // chunk above a store of another), then the selects, then the stores
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int slot = min(i + 32 * (C0 + k) + lane, M - 1) & (DR - 1), rc = max(R.p[k] - 1, q1c);
+      vC[k] = ringV[cs + rc];
+      aC[k] = ringA[cs + rc];
+      vR[k] = runV[slot];
+      aR[k] = runA[slot];
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int pma = R.p[k] - 1 < q1c ? 0 : aC[k];
+      vT[k] = ringV[cs + max(pma - 1, q1c)];  // the row before the minimum's first position
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int jt = i + 32 * (C0 + k) + lane, slot = min(jt, M - 1) & (DR - 1);
+      const bool in = jt < jend;
+      const int p = R.p[k], r = p - 1;
+      const double rv = r < q1c ? s0c : vC[k];
+      const int pma = r < q1c ? 0 : aC[k];
+      const bool first = i == R.qj[k];
+      const double pmj = first ? R.s0j[k] : vR[k];
+      const int paj = first ? 0 : aR[k];
+      const double g = R.g[k];
+      const bool valid = in && g != INF && p > 0;
+      cand[k] = __dadd_rn(rv, g);
+      best[k] = valid ? cand[k] : INF;   // (rv = INF gives cand = INF)
+      const bool lower = best[k] < pmj;  // strict: the first position is kept
+      npm[k] = lower ? best[k] : pmj;
+      na[k] = lower ? i : paj;
+      ws[k] = in ? slot : DR;  // lanes past the row store to the dummy slot
+      wr[k] = in ? slot * DW + (i - R.qj[k]) : DR * DW;
+      const bool fin = valid && cand[k] != INF;
+      bp[k] = fin ? pma : 0xffff;
+      tie[k] = fin && pma > 0 && __dadd_rn(pma - 1 < q1c ? s0c : vT[k], g) == cand[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      runV[ws[k]] = npm[k];
+      runA[ws[k]] = (uint16_t)na[k];
+      ringV[wr[k]] = npm[k];
+      ringA[wr[k]] = (uint16_t)na[k];
+    }
+    bool anytie = false;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) anytie = anytie || tie[k];
+    if (__any_sync(kFull, anytie)) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        if (tie[k]) {  // the first row whose S sums to the same value
+          const double g = R.g[k];
+          int qa = 0, qb = bp[k] - 1;
+          while (qa < qb) {
+            const int mid = (qa + qb) >> 1;
+            if (__dadd_rn(mid < q1c ? s0c : ringV[cs + mid], g) == cand[k]) qb = mid; else qa = mid + 1;
+          }
+          bp[k] = qb;
+        }
+    }
+    const uint32_t xr = xrow(i);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int jt = i + 32 * (C0 + k) + lane;
+      if (jt < jend) {
+        PAR[xr + (uint32_t)jt] = (uint16_t)bp[k];
+        if (jt == M - 1) a.slast[i] = best[k];
+      }
+    }
+  };
+  auto step = [&](const DpIn<NCW>& cur, DpIn<NCW>& nxt, int i) {
+    const int live = ((cur.rl + 31) >> 5) - C0;  // this warp's chunks holding useful cells
+    if (C0 == 0 && lane == 0 && i + cur.rl < M) a.slast[i] = INF;
+    if (live >= NCW) stage(cur, i, std::integral_constant<int, NCW>{});
+    else if (NCW > 1 && live == 1) stage(cur, i, std::integral_constant<int, 1>{});
+    issue(i + kPD);                // into row i's slot (read by fetch(cur, i))
+    cp_async_wait<kPD - 1>();      // row i + 1 has landed
+    fetch(nxt, i + 1);
+    dp_bar();                      // both warps' stores of stage i before stage i + 1's loads
+  };
+  for (int r = 1; r <= kPD; ++r) issue(r);
+  cp_async_wait<kPD - 1>();
+  DpIn<NCW> A, B;
+  fetch(A, 1);
+  for (int i = 1; i < M; i += 2) {
+    step(A, B, i);
+    if (i + 1 >= M) break;
+    step(B, A, i + 1);
+  }
+  cp_async_wait<0>();
+}
+
 __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
   if (*a.status != INT_MAX) return;
   extern __shared__ __align__(16) unsigned char smb[];
-  constexpr int DW = kFastDW, DR = kFastDR;
+  constexpr int DW = kFastDW;
   const int M = a.M, tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
   __shared__ int ired[8];
   int rlmax = 0;
@@ -364,149 +524,9 @@ __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
     for (int c = max(e0, 1); c < e1 && c < M; ++c) q1[c] = (uint16_t)q;
   }
   __syncthreads();
-  if (warp != 0) return;
-  const double* __restrict__ G = a.G;
-  const uint16_t* __restrict__ PF = a.pfit;
-  uint16_t* __restrict__ PAR = a.par;
-  // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j
-  auto xrow = [&](int i) {
-    const uint32_t ui = (uint32_t)i;
-    return ui * (uint32_t)M - ui * (ui - 1u) / 2u - ui;
-  };
-  auto issue = [&](int r) {  // cp.async row r's cells (all three chunks; the row runs to M-1)
-    if (r < M) {
-      const int s = (r & (kPD - 1)) * DW;
-      const uint32_t xr = xrow(r);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const uint32_t x = xr + (uint32_t)min(r + 32 * c + lane, M - 1);
-        cp_async8(stG + s + 32 * c + lane, G + x);
-        cp_async4(stP + s + 32 * c + lane,
-                  reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(PF + x) & ~(uintptr_t)3));
-      }
-    }
-    cp_async_commit();
-  };
-  auto fetch = [&](DpIn& R, int i) {  // row i's inputs into registers (its cp.async group has landed)
-    if (i >= M) return;
-    const int s = (i & (kPD - 1)) * DW;
-    const uint32_t xr = xrow(i);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int j = min(i + 32 * c + lane, M - 1);
-      R.g[c] = stG[s + 32 * c + lane];
-      R.p[c] = i + 32 * c + lane < i + rlS[i]  // past the row's useful cells pfit is not computed
-                   ? (int)((stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu) : 0;
-      R.qj[c] = q1[j];
-      R.s0j[c] = S0[j];
-    }
-    R.rl = rlS[i];
-    R.q1c = q1[i - 1];
-    R.s0c = S0[i - 1];
-  };
-  auto stage = [&](const DpIn& R, int i, auto nc_tag) {
-    constexpr int NC = decltype(nc_tag)::value;
-    const int jend = i + R.rl, q1c = R.q1c;
-    const double s0c = R.s0c;
-    const int cs = ((i - 1) & (DR - 1)) * DW - q1c;  // column i-1: entry of row r at cs + r, r >= q1c
-    double best[NC], cand[NC], vC[NC], vR[NC], npm[NC];
-    int bp[NC], aC[NC], aR[NC], na[NC], ws[NC], wr[NC];
-    bool tie[NC];
-    // all loads of the stage first (the compiler cannot move a load of one
-    // chunk above a store of another), then the selects, then the stores
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int slot = min(i + 32 * c + lane, M - 1) & (DR - 1), rc = max(R.p[c] - 1, q1c);
-      vC[c] = ringV[cs + rc];
-      aC[c] = ringA[cs + rc];
-      vR[c] = runV[slot];
-      aR[c] = runA[slot];
-    }
-    double vT[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int pma = R.p[c] - 1 < q1c ? 0 : aC[c];
-      vT[c] = ringV[cs + max(pma - 1, q1c)];  // the row before the minimum's first position
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int jt = i + 32 * c + lane, slot = min(jt, M - 1) & (DR - 1);
-      const bool in = jt < jend;
-      const int p = R.p[c], r = p - 1;
-      const double rv = r < q1c ? s0c : vC[c];
-      const int pma = r < q1c ? 0 : aC[c];
-      const bool first = i == R.qj[c];
-      const double pmj = first ? R.s0j[c] : vR[c];
-      const int paj = first ? 0 : aR[c];
-      const double g = R.g[c];
-      const bool valid = in && g != INF && p > 0;
-      cand[c] = __dadd_rn(rv, g);
-      best[c] = valid ? cand[c] : INF;   // (rv = INF gives cand = INF)
-      const bool lower = best[c] < pmj;  // strict: the first position is kept
-      npm[c] = lower ? best[c] : pmj;
-      na[c] = lower ? i : paj;
-      ws[c] = in ? slot : DR;  // lanes past the row store to the dummy slot
-      wr[c] = in ? slot * DW + (i - R.qj[c]) : DR * DW;
-      const bool fin = valid && cand[c] != INF;
-      bp[c] = fin ? pma : 0xffff;
-      tie[c] = fin && pma > 0 && __dadd_rn(pma - 1 < q1c ? s0c : vT[c], g) == cand[c];
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      runV[ws[c]] = npm[c];
-      runA[ws[c]] = (uint16_t)na[c];
-      ringV[wr[c]] = npm[c];
-      ringA[wr[c]] = (uint16_t)na[c];
-    }
-    bool anytie = false;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) anytie = anytie || tie[c];
-    if (__any_sync(kFull, anytie)) {
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (tie[c]) {  // the first row whose S sums to the same value
-          const double g = R.g[c];
-          int qa = 0, qb = bp[c] - 1;
-          while (qa < qb) {
-            const int mid = (qa + qb) >> 1;
-            if (__dadd_rn(mid < q1c ? s0c : ringV[cs + mid], g) == cand[c]) qb = mid; else qa = mid + 1;
-          }
-          bp[c] = qb;
-        }
-    }
-    const uint32_t xr = xrow(i);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int jt = i + 32 * c + lane;
-      if (jt < jend) {
-        PAR[xr + (uint32_t)jt] = (uint16_t)bp[c];
-        if (jt == M - 1) a.slast[i] = best[c];
-      }
-    }
-  };
-  auto step = [&](const DpIn& cur, DpIn& nxt, int i) {
-    if (lane == 0 && i + cur.rl < M) a.slast[i] = INF;
-    switch ((cur.rl + 31) >> 5) {
-      case 1: stage(cur, i, std::integral_constant<int, 1>{}); break;
-      case 2: stage(cur, i, std::integral_constant<int, 2>{}); break;
-      case 3: stage(cur, i, std::integral_constant<int, 3>{}); break;
-      default: break;  // no useful cell
-    }
-    issue(i + kPD);                // into row i's slot (read by fetch(cur, i))
-    cp_async_wait<kPD - 1>();      // row i + 1 has landed
-    fetch(nxt, i + 1);
-    __syncwarp();
-  };
-  for (int r = 1; r <= kPD; ++r) issue(r);
-  cp_async_wait<kPD - 1>();
-  DpIn A, B;
-  fetch(A, 1);
-  for (int i = 1; i < M; i += 2) {
-    step(A, B, i);
-    if (i + 1 >= M) break;
-    step(B, A, i + 1);
-  }
-  cp_async_wait<0>();
+  const DpPtrs sp{S0, ringV, runV, stG, ringA, runA, q1, rlS, stP};
+  if (warp == 0) dp_warp<0, 1>(a, sp, lane);       // cells i .. i+31 of each row
+  else if (warp == 1) dp_warp<1, 2>(a, sp, lane);  // cells i+32 .. i+95
 }
 
 template <int N>
@@ -993,7 +1013,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
         for (int n = 0; n <= N; ++n) t[n] = 0.0;
       }
       const int nu = min(32, hi - x0 + 1);
-      for (int u = 0; u < nu; ++u) {
+      auto member = [&](int u) {  // member x0 + u's terms onto the running total
         const int su = __shfl_sync(kFull, sp, u);
 #pragma unroll
         for (int n = 1; n <= N; ++n) {
@@ -1002,6 +1022,12 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
         }
         const double up = __shfl_sync(kFull, t[N], u);
         if (su < N) total = __dadd_rn(total, up);
+      };
+      if (nu == 32) {  // unrolled: the shuffles run ahead of the serial adds
+#pragma unroll
+        for (int u = 0; u < 32; ++u) member(u);
+      } else {
+        for (int u = 0; u < nu; ++u) member(u);
       }
 #pragma unroll
       for (int n = 1; n <= N; ++n) cnt[n - 1] += __popc(__ballot_sync(kFull, live && sp < n));
