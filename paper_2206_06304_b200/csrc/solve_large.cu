@@ -272,23 +272,25 @@ extern "C" int coinfer_debug_large_times(unsigned long long* out) {
 }
 #endif
 // The grouping DP when every row i >= 1 has <= kFastDW useful cells (C4:
-// ~35, peaks in the 70s), one warp, one row per stage (offline_solvers.hpp:
-// 313-330).  Column c's useful rows are row 0 and a suffix [q1(c), c], so
+// ~35, peaks in the 70s), one row per stage (offline_solvers.hpp:313-330).  Column c's useful rows are row 0 and a suffix [q1(c), c], so
 // its prefix minima live dense over that suffix: S0[c] (row 0) below
 // q1(c), then one entry per row; only columns i-1 .. i+DW are live at
 // stage i, so they sit in a ring of DR column slots.
 //   Stage i needs column i-1 complete and nothing else new: its critical
 // path is one shared load of column i-1 and of each cell's running
-// minimum, an add, a compare and the stores.  One warp runs it, so every
-// dependency is exposed: the stage is straight-line code over only the
+// minimum, an add, a compare and the stores.  Two warps run it (32 and 64
+// cells of the row), so every dependency is exposed: the stage is
+// straight-line code over only the
 // row's live 32-cell chunks (stores of lanes past the row go to a dummy
 // slot instead of branching), the parent's tie check (rounding that merges
 // an earlier, larger S into the same sum) reads column i-1 beside the
-// critical chain, and the row's G / pfit come from a shared-memory ring
-// that cp.async fills kPD rows ahead (the completion counter, not a
-// register scoreboard, tracks them), read into registers one stage ahead.
+// critical chain, and the rows' G / pfit are staged by cp.async in a
+// producer warp (dp_producer), which hands each stage a record (G, pfit
+// masked to the useful cells, the column's q1) two stages ahead.
 namespace {
-constexpr int kPD = 8;  // rows of G / pfit in flight (power of 2)
+constexpr int kPD = 4;  // rows of G / pfit in flight (power of 2)
+constexpr int kQ = 4;   // stage records in the ring the producer warp fills (power of 2)
+constexpr int kDpSmemMax = 227 * 1024;  // large_dp runs when its shared memory fits (M <= ~8,000)
 template <int NW>
 struct DpIn {  // one stage's inputs, per lane: cells i + 32(C0 + k) + lane of this warp's chunks
   double g[NW], s0j[NW];
@@ -297,11 +299,12 @@ struct DpIn {  // one stage's inputs, per lane: cells i + 32(C0 + k) + lane of t
   double s0c;
 };
 struct DpPtrs {  // large_dp's shared-memory arrays
-  double *S0, *ringV, *runV, *stG;
+  double *S0, *ringV, *runV, *stG, *recG, *recS0c;
   uint16_t *ringA, *runA, *q1, *rlS;
-  uint32_t* stP;
+  uint32_t *stP, *recPQ;
+  int* recRl;  // [kQ] row length, [kQ] q1(i-1)
 };
-__device__ __forceinline__ void dp_bar() { asm volatile("bar.sync 1, 64;" : : : "memory"); }
+__device__ __forceinline__ void dp_bar() { asm volatile("bar.sync 1, 96;" : : : "memory"); }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" : : "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -317,7 +320,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (+1 dummy) | ring positions | running positions | q1 | rlen | staged G |
 // staged pfit words
 struct DpSmem {
-  int oRingV, oRunV, oRingA, oRunA, oQ1, oRl, oStG, oStP, bytes;
+  int oRingV, oRunV, oRingA, oRunA, oQ1, oRl, oStG, oStP, oRecG, oRecPQ, oRecS0c, oRecRl, bytes;
   __host__ __device__ explicit DpSmem(int M) {
     auto al = [](int x) { return (x + 15) & ~15; };
     oRingV = al(8 * M);
@@ -328,12 +331,75 @@ struct DpSmem {
     oRl = al(oQ1 + 2 * M);
     oStG = al(oRl + 2 * M);
     oStP = al(oStG + 8 * kPD * kFastDW);
-    bytes = al(oStP + 4 * kPD * kFastDW);
+    oRecG = al(oStP + 4 * kPD * kFastDW);
+    oRecPQ = al(oRecG + 8 * kQ * kFastDW);
+    oRecS0c = al(oRecPQ + 4 * kQ * kFastDW);
+    oRecRl = al(oRecS0c + 8 * kQ);
+    bytes = al(oRecRl + 8 * kQ);
   }
 };
 }  // namespace
 
-// One of large_dp's two warps: chunks C0 .. C0+NCW-1 (32 cells each) of
+// large_dp's producer warp: G and pfit rows staged by cp.async kPD rows
+// ahead (kPD), and per row the stage record the DP warps read -- each cell's G
+// and (pfit masked to the row's useful cells | q1 of its column), the row
+// length, q1(i-1), S0[i-1] -- into a ring of kQ records, two rows ahead of
+// the stage that reads them (one named barrier per stage orders both).
+__device__ __forceinline__ void dp_producer(const LargeArgs& a, const DpPtrs& sp, int lane) {
+  constexpr int DW = kFastDW;
+  const int M = a.M;
+  const double* __restrict__ G = a.G;
+  const uint16_t* __restrict__ PF = a.pfit;
+  auto xrow = [&](int i) {
+    const uint32_t ui = (uint32_t)i;
+    return ui * (uint32_t)M - ui * (ui - 1u) / 2u - ui;
+  };
+  auto issue = [&](int r) {
+    if (r < M) {
+      const int s = (r & (kPD - 1)) * DW;
+      const uint32_t xr = xrow(r);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t x = xr + (uint32_t)min(r + 32 * c + lane, M - 1);
+        cp_async8(sp.stG + s + 32 * c + lane, G + x);
+        cp_async4(sp.stP + s + 32 * c + lane,
+                  reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(PF + x) & ~(uintptr_t)3));
+      }
+    }
+    cp_async_commit();
+  };
+  auto produce = [&](int r) {  // record of row r (1 <= r < M)
+    issue(r + kPD - 1);
+    cp_async_wait<kPD - 1>();  // row r has landed
+    const int s = (r & (kPD - 1)) * DW, q = (r & (kQ - 1)) * DW;
+    const uint32_t xr = xrow(r);
+    const int rl = sp.rlS[r];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int jt = r + 32 * c + lane, j = min(jt, M - 1);
+      const uint32_t pw = jt < r + rl  // past the row's useful cells pfit is not computed
+                              ? (sp.stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu : 0u;
+      sp.recG[q + 32 * c + lane] = sp.stG[s + 32 * c + lane];
+      sp.recPQ[q + 32 * c + lane] = pw | ((uint32_t)sp.q1[j] << 16);
+    }
+    if (lane == 0) {
+      sp.recRl[r & (kQ - 1)] = rl;
+      sp.recRl[kQ + (r & (kQ - 1))] = sp.q1[r - 1];
+      sp.recS0c[r & (kQ - 1)] = sp.S0[r - 1];
+    }
+  };
+  for (int r = 1; r < kPD; ++r) issue(r);
+  produce(1);
+  if (2 < M) produce(2);
+  dp_bar();  // records 1 and 2
+  for (int i = 1; i < M; ++i) {
+    if (i + 2 < M) produce(i + 2);
+    dp_bar();  // end of stage i
+  }
+  cp_async_wait<0>();
+}
+
+// One of large_dp's two DP warps: chunks C0 .. C0+NCW-1 (32 cells each) of
 // every row; the warps meet at a named barrier after each stage (a stage
 // reads ring entries the other warp wrote in the stages before).
 template <int C0, int NCW>
@@ -345,45 +411,27 @@ __device__ __forceinline__ void dp_warp(const LargeArgs& a, const DpPtrs& sp, in
   double* __restrict__ runV = sp.runV;
   uint16_t* __restrict__ ringA = sp.ringA;
   uint16_t* __restrict__ runA = sp.runA;
-  const double* __restrict__ G = a.G;
-  const uint16_t* __restrict__ PF = a.pfit;
   uint16_t* __restrict__ PAR = a.par;
   // 32-bit triangle offsets (M <= 8192: < 2^26 cells): x(i, j) = xr(i) + j
   auto xrow = [&](int i) {
     const uint32_t ui = (uint32_t)i;
     return ui * (uint32_t)M - ui * (ui - 1u) / 2u - ui;
   };
-  auto issue = [&](int r) {  // cp.async this warp's cells of row r (the row runs to M-1)
-    if (r < M) {
-      const int s = (r & (kPD - 1)) * DW;
-      const uint32_t xr = xrow(r);
-#pragma unroll
-      for (int k = 0; k < NCW; ++k) {
-        const int c = C0 + k;
-        const uint32_t x = xr + (uint32_t)min(r + 32 * c + lane, M - 1);
-        cp_async8(sp.stG + s + 32 * c + lane, G + x);
-        cp_async4(sp.stP + s + 32 * c + lane,
-                  reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(PF + x) & ~(uintptr_t)3));
-      }
-    }
-    cp_async_commit();
-  };
-  auto fetch = [&](DpIn<NCW>& R, int i) {  // row i's inputs into registers (its cp.async group has landed)
+  auto fetch = [&](DpIn<NCW>& R, int i) {  // row i's stage record into registers
     if (i >= M) return;
-    const int s = (i & (kPD - 1)) * DW;
-    const uint32_t xr = xrow(i);
-    R.rl = sp.rlS[i];
+    const int q = (i & (kQ - 1)) * DW;
+    R.rl = sp.recRl[i & (kQ - 1)];
+    R.q1c = sp.recRl[kQ + (i & (kQ - 1))];
+    R.s0c = sp.recS0c[i & (kQ - 1)];
 #pragma unroll
     for (int k = 0; k < NCW; ++k) {
-      const int c = C0 + k, jt = i + 32 * c + lane, j = min(jt, M - 1);
-      R.g[k] = sp.stG[s + 32 * c + lane];
-      R.p[k] = jt < i + R.rl  // past the row's useful cells pfit is not computed
-                   ? (int)((sp.stP[s + 32 * c + lane] >> (((xr + (uint32_t)j) & 1u) * 16u)) & 0xffffu) : 0;
-      R.qj[k] = sp.q1[j];
-      R.s0j[k] = sp.S0[j];
+      const int c = C0 + k;
+      const uint32_t pq = sp.recPQ[q + 32 * c + lane];
+      R.g[k] = sp.recG[q + 32 * c + lane];
+      R.p[k] = (int)(pq & 0xffffu);
+      R.qj[k] = (int)(pq >> 16);
+      R.s0j[k] = sp.S0[min(i + 32 * c + lane, M - 1)];
     }
-    R.q1c = sp.q1[i - 1];
-    R.s0c = sp.S0[i - 1];
   };
   auto stage = [&](const DpIn<NCW>& R, int i, auto nc_tag) {
     constexpr int NC = decltype(nc_tag)::value;  // live chunks of this warp
@@ -469,13 +517,10 @@ __device__ __forceinline__ void dp_warp(const LargeArgs& a, const DpPtrs& sp, in
     if (C0 == 0 && lane == 0 && i + cur.rl < M) a.slast[i] = INF;
     if (live >= NCW) stage(cur, i, std::integral_constant<int, NCW>{});
     else if (NCW > 1 && live == 1) stage(cur, i, std::integral_constant<int, 1>{});
-    issue(i + kPD);                // into row i's slot (read by fetch(cur, i))
-    cp_async_wait<kPD - 1>();      // row i + 1 has landed
-    fetch(nxt, i + 1);
+    fetch(nxt, i + 1);             // written by the producer before the last barrier
     dp_bar();                      // both warps' stores of stage i before stage i + 1's loads
   };
-  for (int r = 1; r <= kPD; ++r) issue(r);
-  cp_async_wait<kPD - 1>();
+  dp_bar();  // records 1 and 2
   DpIn<NCW> A, B;
   fetch(A, 1);
   for (int i = 1; i < M; i += 2) {
@@ -483,7 +528,6 @@ __device__ __forceinline__ void dp_warp(const LargeArgs& a, const DpPtrs& sp, in
     if (i + 1 >= M) break;
     step(B, A, i + 1);
   }
-  cp_async_wait<0>();
 }
 
 __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
@@ -499,7 +543,7 @@ __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
   __syncthreads();
   rlmax = 0;
   for (int w = 0; w < NW; ++w) rlmax = max(rlmax, ired[w]);
-  if (rlmax > DW) return;  // large_finish runs the change-point DP
+  if (rlmax > DW || DpSmem(M).bytes > kDpSmemMax) return;  // large_finish runs the change-point DP
   const double INF = dinf();
   const DpSmem L(M);
   double* S0 = reinterpret_cast<double*>(smb);                   // [M] row 0: S = G = PM
@@ -524,9 +568,13 @@ __global__ void __launch_bounds__(256) large_dp(LargeArgs a) {
     for (int c = max(e0, 1); c < e1 && c < M; ++c) q1[c] = (uint16_t)q;
   }
   __syncthreads();
-  const DpPtrs sp{S0, ringV, runV, stG, ringA, runA, q1, rlS, stP};
+  const DpPtrs sp{S0, ringV, runV, stG,
+                  reinterpret_cast<double*>(smb + L.oRecG), reinterpret_cast<double*>(smb + L.oRecS0c),
+                  ringA, runA, q1, rlS, stP, reinterpret_cast<uint32_t*>(smb + L.oRecPQ),
+                  reinterpret_cast<int*>(smb + L.oRecRl)};
   if (warp == 0) dp_warp<0, 1>(a, sp, lane);       // cells i .. i+31 of each row
   else if (warp == 1) dp_warp<1, 2>(a, sp, lane);  // cells i+32 .. i+95
+  else if (warp == 2) dp_producer(a, sp, lane);    // G / pfit staging and the stage records
 }
 
 template <int N>
@@ -644,7 +692,7 @@ __global__ void __launch_bounds__(1024) large_finish(LargeArgs a) {
   rlmax = 0;
   for (int w = 0; w < NW; ++w) rlmax = max(rlmax, ired[w]);
   __syncthreads();
-  const bool fastdp = rlmax <= kFastDW;
+  const bool fastdp = rlmax <= kFastDW && DpSmem(M).bytes <= kDpSmemMax;  // (the test large_dp made)
   if (fastdp) {
     // the whole DP ran in large_dp (same rlmax test): S row M-1 in slast, parents in par
   } else {
@@ -1103,9 +1151,9 @@ static cudaError_t launch_large_n(LargeArgs a, cudaStream_t st) {
   const int smem_fast = DpSmem(M).bytes;  // large_dp
   // large_finish: running PM, staged column | ring (128 x 16 points + owners) | counts, staged rows, rlen, last rows
   const int smem = 8 * 2 * M + 128 * 16 * 10 + 128 * 4 + 2 * 4 * M;
-  if (M > 8 * 1024 || smem > 227 * 1024 || smem_fast > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
+  if (M > 8 * 1024 || smem > 227 * 1024) return cudaErrorInvalidValue;  // <= 8 DP cells per thread
   cudaError_t e;
-  if (a.do_og) {
+  if (a.do_og && smem_fast <= kDpSmemMax) {
     e = ensure_smem((const void*)large_dp, smem_fast);
     if (e != cudaSuccess) return e;
     large_dp<<<1, 256, smem_fast, st>>>(a);
