@@ -120,3 +120,47 @@ def test_c4_shape_properties(engine):
     assert e == og["energy"][0]
     assert og["group_size"][0][:g].sum() == M
     assert (np.diff(og["group_deadline"][0][:g]) >= 0).all()
+
+
+def test_fast_dp_all_chunks_vs_oracle(engine):
+    """Deadlines U[0.3, 1.5] at M = 300: every row keeps <= 96 useful cells
+    but ~70 rows keep more than 64, so large_dp's second DP warp runs both
+    of its chunks (cells i+32..i+95) and the 1-/2-chunk stage variants
+    alternate; decisions bit-exact against the oracle."""
+    M = 300
+    prof = profile_heavy(M)
+    users = sample_batch(2, M, prof, 0.3, 1.5, seed=1)
+    sl = np.zeros(M + 1)
+    for n in range(prof.N):
+        sl[1:] = sl[1:] + prof.latency[n][:M]
+    for k in range(2):
+        dl = np.sort(users["deadline"][k])
+        rlen = [int(np.sum(dl[0] + sl[1:M - i + 1] <= dl[i])) for i in range(1, M)]
+        assert max(rlen) <= 96 and sum(r > 64 for r in rlen) > 30
+    ip, og = engine.sweep(prof, users)
+    ck.assert_same_ip(ip, ck.oracle_ipssa(prof, users), where="fast dp ipssa")
+    ck.assert_same_og(og, ck.oracle_og(prof, users), where="fast dp og")
+
+
+@pytest.mark.parametrize("M", [7000, 8000])
+def test_large_dp_shared_memory_limit(engine, M):
+    """Near the largest sizes: at M = 7000 large_dp's shared memory (dense
+    prefix-minimum ring + S0/q1/rlen per user) fits 227 KB, at M = 8000 it
+    does not and large_finish runs the change-point DP instead.  Both
+    plans are internally consistent (energy = left fold of the group
+    energies, groups cover the users in deadline order, every user's
+    energy and batch counts add up)."""
+    prof = profile_heavy(M)
+    users = sample_batch(1, M, prof, 0.25, 1.0, seed=M)
+    og = engine.og(prof, users)
+    assert og["status"][0] == 0 and og["fallback"][0] == 0
+    g = og["n_groups"][0]
+    e = 0.0
+    for x in og["group_energy"][0][:g]:
+        e += x
+    assert e == og["energy"][0]
+    assert og["group_size"][0][:g].sum() == M
+    assert (np.diff(og["group_lo"][0][:g]) > 0).all() and og["group_lo"][0][0] == 0
+    assert (np.diff(og["group_deadline"][0][:g]) >= 0).all()
+    gu = og["group_of_user"][0]
+    assert np.bincount(gu, minlength=g)[:g].tolist() == og["group_size"][0][:g].tolist()
