@@ -1,5 +1,8 @@
 """The large-instance path (solve_large.cu: global-memory G/S, one warp per
-row, single-CTA DP) — BASELINE config 4 (M = 4096 in one instance).
+row; the DP in large_dp -- two DP warps and a producer warp -- when every
+row has <= 96 useful cells and its shared memory fits, else the
+change-point DP of large_finish) — BASELINE config 4 (M = 4096 in one
+instance).
 
 Parity: vs the C oracle at M in the hundreds, and vs the (fixture-validated)
 shared-memory path on many small instances by forcing the large path."""
