@@ -278,10 +278,12 @@ void patch_og_out(unsigned char* b, coinfer_og_out& o) {
 }
 
 #ifndef CFB_E2E_CHUNKS
-#define CFB_E2E_CHUNKS 32  // host-memory batches: up to this many chunks pipelined over two streams
+#define CFB_E2E_CHUNKS 64  // host-memory batches: up to this many chunks pipelined over two streams
 #endif
 #ifndef CFB_E2E_MINCHUNK
-#define CFB_E2E_MINCHUNK 32768  // instances per chunk, at least (measured: 8 / 16 / 32 chunks of 1M: 8.17 / 8.40 / 8.53M/s e2e)
+// instances per chunk, at least (measured, 1M C3 instances: 8 / 16 / 32 chunks 8.17 / 8.40 / 8.53M/s e2e
+// in round 1; 32 / 64 / 128 chunks 11.25 / 11.31 / 11.21M/s e2e on the round-2 kernel)
+#define CFB_E2E_MINCHUNK 16384
 #endif
 constexpr int kSmallMaxM = 255;
 #ifndef CFB_PIPE_MAXM

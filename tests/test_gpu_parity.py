@@ -223,8 +223,9 @@ def test_device_and_host_paths_agree(engine):
 
 
 def test_host_pipeline_chunks_agree_with_device(engine):
-    """Host batches of >= 131072 instances go through the chunked two-stream
-    pipeline (up to 32 chunks); their results must equal one device launch."""
+    """Host batches of >= 65536 instances go through the chunked two-stream
+    pipeline (up to 64 chunks of >= 16384); their results must equal one
+    device launch."""
     import torch
     prof = profile_heavy(12)
     users = sample_batch(140_000, 12, prof, 0.25, 1.0, seed=13)
