@@ -35,7 +35,8 @@ namespace cfb {
 #endif
 #ifndef CFB_PIPE_GW1
 #define CFB_PIPE_GW1 16  // when one CTA of two buffers fits an SM: 24 warps (M=100 target,
-#endif                   // 100k instances: 20+4 / 18+6 / 16+8 / 14+10 -> 45.1 / 43.3 / 42.6 / 42.3 ms)
+#endif                   // 100k instances: 20+4 / 18+6 / 16+8 / 14+10 -> 45.1 / 43.3 / 42.6 / 42.3 ms;
+                         // 28 warps 18+10: 42.0 vs 42.0, 32 warps 20+12: 43.3)
 #ifndef CFB_PIPE_LW1
 #define CFB_PIPE_LW1 8
 #endif
