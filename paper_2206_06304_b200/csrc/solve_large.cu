@@ -513,11 +513,13 @@ __device__ __forceinline__ void dp_warp(const LargeArgs& a, const DpPtrs& sp, in
     }
   };
   auto step = [&](const DpIn<NCW>& cur, DpIn<NCW>& nxt, int i) {
+    // the next stage's record first (the producer wrote it before the last
+    // barrier): its loads then run beside this stage's chain
+    fetch(nxt, i + 1);
     const int live = ((cur.rl + 31) >> 5) - C0;  // this warp's chunks holding useful cells
     if (C0 == 0 && lane == 0 && i + cur.rl < M) a.slast[i] = INF;
     if (live >= NCW) stage(cur, i, std::integral_constant<int, NCW>{});
     else if (NCW > 1 && live == 1) stage(cur, i, std::integral_constant<int, 1>{});
-    fetch(nxt, i + 1);             // written by the producer before the last barrier
     dp_bar();                      // both warps' stores of stage i before stage i + 1's loads
   };
   dp_bar();  // records 1 and 2
